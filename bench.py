@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""STFAS V-cycle throughput on B200 (BASELINE.json metric).
+
+metric: spacetime cell-updates/s = n^d * N / (seconds per FAS V-cycle), with
+s/V-cycle and HBM GB/s reported beside it.  A "step" is one full STFAS
+V-cycle (all levels, PAPER Alg. 2) over the whole spacetime volume, inputs
+resident in HBM.  Default workload: BASELINE config 5 (3D 128^3 x 80 fp32,
+4 levels), the config the metric's 1/2/4/8-GPU scaling is quoted on.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
+    python bench.py --impl reference ...   # CPU oracle (port) on host cores
+
+Multi-GPU (N>1, torchrun): every rank solves its own replica of the workload
+("replicas", weak scaling) -- DESIGN.md §6 explains why the time-slab split
+is not yet the default.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# bytes per cell-timestep moved by one smoother sweep: read and
+# write the state (s = 2d+2 values) and read the guide (d values)
+def sweep_values(dim):
+    s = 2 * dim + 2
+    return 2 * s + dim
+
+
+def vcycle_values_per_cts(dim, levels):
+    """SURVEY.md §8d algorithmic values per fine cell-timestep per V-cycle."""
+    s, g = 2 * dim + 2, dim
+    r = s
+    per = {}
+    l0 = 4 * (2 * s + g) + (s + s / 2 ** dim) + (s + g + s / 2 ** dim) + (2 * s / 2 ** dim + 2 * s)
+    lmid = 4 * (2 * s + g + r) + (s + s / 2 ** dim) + (s + g + r + s / 2 ** dim) + (2 * s / 2 ** dim + 2 * s) \
+        + (3 * s + g)
+    coarsest = 10 * (2 * s + g + r) + (3 * s + g)
+    tot = 0.0
+    for l in range(levels):
+        w = 2.0 ** (-dim * l)
+        if l == levels - 1:
+            tot += w * coarsest
+        elif l == 0:
+            tot += w * l0
+        else:
+            tot += w * lmid
+    return tot
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.strip().split(",") for r in self.f.read().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample_shape(w):
+    """Bounded same-family sample the CPU oracle can finish in ~10-30 s."""
+    if w.dim == 3:
+        return dict(dim=3, n=16, N=8, levels=min(w.levels, 3))
+    return dict(dim=2, n=32, N=min(w.N, 16), levels=min(w.levels, 2))
+
+
+def cpu_vcycle_rate(w, steps=1):
+    """Time the oracle (numpy fp64 port) V-cycle on the host; cell-updates/s."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle import stfas
+    from problems import make_problem
+    sh = cpu_sample_shape(w)
+    pb = make_problem(sh["dim"], n=sh["n"], N=sh["N"], K=w.K, r=w.r, seed=3)
+    levels = stfas.build_levels(pb, sh["levels"])
+    st = stfas.zero_state(pb.g, pb.N)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = stfas.gauge_fix(stfas.vcycle(levels, 0, st))
+    dt = (time.perf_counter() - t0) / steps
+    cts = sh["n"] ** sh["dim"] * sh["N"]
+    return cts / dt, dt, sh
+
+
+def run_reference(args, w, rank, world):
+    if rank != 0:
+        return 0
+    steps, warm = args.steps, args.warmup
+    rate_s = []
+    sh = None
+    for i in range(warm + steps):
+        r, dt, sh = cpu_vcycle_rate(w, 1)
+        if i >= warm:
+            rate_s.append((r, dt))
+    val = sum(r for r, _ in rate_s) / len(rate_s)
+    ms = 1000.0 * sum(d for _, d in rate_s) / len(rate_s)
+    sample = (f"oracle fp64 numpy FAS V-cycle on a same-family {sh['n']}^{sh['dim']} x {sh['N']} "
+              f"({sh['levels']} levels) problem; rate per cell-timestep")
+    line = {
+        "impl": "reference", "metric": "STFAS spacetime cell-updates/s (per V-cycle)", "value": val,
+        "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "config_index": w.index, "cell_timesteps": w.cell_timesteps,
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": val, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--dtype", default=None, choices=[None, "fp32", "fp64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    from paper_1608_01102_b200 import workloads
+    dt_override = {"fp32": torch.float32, "fp64": torch.float64}.get(args.dtype)
+    w = workloads.config(args.config, dt_override)
+
+    if args.impl == "reference":
+        return run_reference(args, w, rank, world)
+
+    import torch.distributed as dist
+    from paper_1608_01102_b200 import _lib, nso
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    L = _lib.load()
+
+    spec = w.spec
+    vstar = workloads.guide_velocity(w)
+    v0 = workloads.initial_velocity(w)
+    cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=w.levels)
+    state = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
+    hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
+    hier.set_guide(v0, vstar)
+    stream = torch.cuda.current_stream()
+
+    # inputs larger than L2 (126 MB) for configs >= 3; otherwise flush L2
+    state_bytes = sum(t.numel() * t.element_size() for t in (*state.V, state.PB, *state.U, state.P))
+    guide_bytes = sum(t.numel() * t.element_size() for t in vstar)
+    flush = None
+    if state_bytes + guide_bytes < 4 * 126e6:
+        flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        hier.vcycle(state)
+        hier.gauge_fix(state)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device events) ----------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local) if rank == 0 else None
+    hier.profile(True)
+    n0 = L.smk_launch_count()
+    t_total = 0.0
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        hier.vcycle(state)
+        hier.gauge_fix(state)
+        e1.record(stream)
+        e1.synchronize()
+        t_total += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    launches = L.smk_launch_count() - n0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    k_ms, k_n, k_cells = hier.profile_read()
+    hier.profile(False)
+    ms = t_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    ri, r2 = hier.residual_norms(state)
+    value = w.cell_timesteps * world / (ms / 1000.0)
+    hbm, peak_kind = peaks()
+    esz = 4 if w.dtype == torch.float32 else 8
+    # dominant kernel: the smoother's colour kernel
+    k_bytes = k_cells * sweep_values(w.dim) * esz / (2 ** w.dim)   # per colour launch share of a sweep
+    k_avg_ms = k_ms / max(k_n, 1)
+    k_achieved = (k_bytes / max(k_n, 1)) / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
+    vc_bytes = vcycle_values_per_cts(w.dim, hier.levels) * esz * w.cell_timesteps
+    vc_gbs = vc_bytes / (ms / 1000.0) / 1e9
+
+    # ---------------- end to end through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda t: t.detach().cpu().pin_memory()
+        h_vs = [pin(t) for t in vstar]
+        h_st = [pin(t) for t in (*state.V, state.PB, *state.U, state.P)]
+        d_st = [t for t in (*state.V, state.PB, *state.U, state.P)]
+        out_h = [torch.empty_like(t) for t in h_st]
+        out_h = [t.pin_memory() for t in out_h]
+        h2d = sum(t.numel() * t.element_size() for t in h_vs + h_st)
+        d2h = sum(t.numel() * t.element_size() for t in out_h)
+        e_ms = 0.0
+        for _ in range(max(1, min(args.steps, 3))):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for d, h in zip(vstar, h_vs):
+                d.copy_(h, non_blocking=True)
+            for d, h in zip(d_st, h_st):
+                d.copy_(h, non_blocking=True)
+            hier.set_guide(v0, vstar)
+            hier.vcycle(state)
+            hier.gauge_fix(state)
+            for h, d in zip(out_h, d_st):
+                h.copy_(d, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            e_ms += e0.elapsed_time(e1)
+        e_ms /= max(1, min(args.steps, 3))
+        e2e = {"value": w.cell_timesteps * world / (e_ms / 1000.0), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rate, dt, sh = cpu_vcycle_rate(w, 1)
+            cpu = {"value": rate, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+                   "sample": f"oracle fp64 numpy V-cycle, same-family {sh['n']}^{sh['dim']} x {sh['N']} "
+                             f"({sh['levels']} levels), {dt:.1f} s; numpy stencils single-threaded"}
+        except Exception as ex:  # never fail the GPU line on the CPU leg
+            cpu = {"value": None, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": "STFAS spacetime cell-updates/s (per V-cycle)",
+            "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "s_per_vcycle": ms / 1000.0,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if w.dtype == torch.float32 else "f64", "data": "synthetic",
+            "config": {"workload": w.name, "config_index": w.index, "grid": f"{w.n}^{w.dim}", "frames": w.N,
+                       "levels": hier.levels, "cell_timesteps": w.cell_timesteps,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed" if flush is not None else "inputs larger than L2",
+                       "residual_inf_after": ri},
+            "roofline": {"bound": "hbm", "kernel": "k_scgs_color", "achieved": k_achieved, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": k_achieved / hbm,
+                         "traffic": None, "avg_launch_ms": k_avg_ms, "launches": k_n,
+                         "share_of_step": (k_ms / args.steps) / ms if ms else None},
+            "vcycle_hbm": {"achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
+                           "algorithmic_bytes": vc_bytes},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    hier.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,246 @@
+// Shared device machinery for the STFAS kernels (sm_100a).
+//
+// Layout (identical to the reference's numpy arrays, fields.py:92-133, so the
+// C-ABI is a zero-copy drop-in): every field is a C-order array with an
+// optional leading frame axis.  A cell field is (N, n0, n1[, n2]); face
+// component k is (N, f0, f1[, f2]) with f_a = n_a + (a == k && neumann).
+// 2D grids are handled as 3D with n2 == 1 and no k == 2 component, which keeps
+// every offset computation identical to numpy's.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace smk {
+
+struct Geo {
+  int dim;
+  int n[3];        // cells per axis (n[2] == 1 for 2D)
+  double h;
+  int periodic;
+};
+
+// ---------------------------------------------------------------------------
+// index helpers (templated on DIM / periodicity so the branches fold away)
+// ---------------------------------------------------------------------------
+
+template <int DIM, bool PER>
+struct Ix {
+  int n0, n1, n2;
+  __host__ __device__ Ix(const Geo& g) : n0(g.n[0]), n1(g.n[1]), n2(DIM == 3 ? g.n[2] : 1) {}
+  __host__ __device__ __forceinline__ int n(int a) const { return a == 0 ? n0 : (a == 1 ? n1 : n2); }
+  // extent of face component k along axis a
+  __host__ __device__ __forceinline__ int fe(int k, int a) const { return n(a) + ((!PER && a == k) ? 1 : 0); }
+  __host__ __device__ __forceinline__ int64_t cells() const { return (int64_t)n0 * n1 * n2; }
+  __host__ __device__ __forceinline__ int64_t faces(int k) const {
+    return (int64_t)fe(k, 0) * fe(k, 1) * (DIM == 3 ? fe(k, 2) : 1);
+  }
+  __host__ __device__ __forceinline__ int64_t cell_off(int i, int j, int l) const {
+    return ((int64_t)i * n1 + j) * n2 + l;
+  }
+  __host__ __device__ __forceinline__ int64_t face_off(int k, int i, int j, int l) const {
+    return ((int64_t)i * fe(k, 1) + j) * (DIM == 3 ? fe(k, 2) : 1) + l;
+  }
+  __host__ __device__ __forceinline__ static int wrap(int i, int n) {
+    return i < 0 ? i + n : (i >= n ? i - n : i);
+  }
+  // bounds-checked reads: zero outside (Neumann) / wrapped (periodic)
+  template <class R>
+  __device__ __forceinline__ R face(const R* p, int k, int i, int j, int l) const {
+    if (PER) {
+      i = wrap(i, n0); j = wrap(j, n1); if (DIM == 3) l = wrap(l, n2);
+    } else {
+      if (i < 0 || j < 0 || l < 0 || i >= fe(k, 0) || j >= fe(k, 1) || (DIM == 3 && l >= fe(k, 2))) return R(0);
+    }
+    return p[face_off(k, i, j, DIM == 3 ? l : 0)];
+  }
+  template <class R>
+  __device__ __forceinline__ R cell(const R* p, int i, int j, int l) const {
+    if (PER) {
+      i = wrap(i, n0); j = wrap(j, n1); if (DIM == 3) l = wrap(l, n2);
+    } else {
+      if (i < 0 || j < 0 || l < 0 || i >= n0 || j >= n1 || (DIM == 3 && l >= n2)) return R(0);
+    }
+    return p[cell_off(i, j, DIM == 3 ? l : 0)];
+  }
+  // decode a flat face index of component k
+  __device__ __forceinline__ void face_idx(int k, int64_t o, int c[3]) const {
+    int e2 = DIM == 3 ? fe(k, 2) : 1, e1 = fe(k, 1);
+    c[2] = (int)(o % e2); o /= e2;
+    c[1] = (int)(o % e1); o /= e1;
+    c[0] = (int)o;
+  }
+  __device__ __forceinline__ void cell_idx(int64_t o, int c[3]) const {
+    c[2] = (int)(o % n2); o /= n2;
+    c[1] = (int)(o % n1); o /= n1;
+    c[0] = (int)o;
+  }
+  // wall face of component k at index c (never true for periodic)
+  __device__ __forceinline__ bool wall(int k, const int c[3]) const {
+    return !PER && (c[k] == 0 || c[k] == n(k));
+  }
+};
+
+template <class R>
+struct Face3 {  // per-frame pointers to the d face components
+  const R* c[3];
+};
+
+// Field accessors used by the point stencils: plain memory, or a unit vector.
+template <int DIM, bool PER, class R>
+struct MemField {
+  const Ix<DIM, PER>& ix;
+  Face3<R> f;
+  __device__ __forceinline__ R operator()(int k, int i, int j, int l) const { return ix.face(f.c[k], k, i, j, l); }
+};
+
+template <int DIM, bool PER, class R>
+struct UnitField {  // e_{(k*, c*)}: 1 at one face (indices already canonical)
+  const Ix<DIM, PER>& ix;
+  int k0, i0, j0, l0;
+  __device__ __forceinline__ R operator()(int k, int i, int j, int l) const {
+    if (k != k0) return R(0);
+    if (PER) { i = Ix<DIM, PER>::wrap(i, ix.n0); j = Ix<DIM, PER>::wrap(j, ix.n1); if (DIM == 3) l = Ix<DIM, PER>::wrap(l, ix.n2); }
+    return (i == i0 && j == j0 && (DIM == 2 || l == l0)) ? R(1) : R(0);
+  }
+};
+
+__device__ __forceinline__ void shift(int c[3], int a, int s, int out[3]) {
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[a] += s;
+}
+
+// ---------------------------------------------------------------------------
+// S(a, w)_j at one j-face f  (advection.py:306-365)
+//   S_j = (1/2h) sum_k (A+_{jk} w_j[f+e_k] - A-_{jk} w_j[f-e_k]),  wall-masked.
+// ---------------------------------------------------------------------------
+template <int DIM, bool PER, class R, class FA, class FW>
+__device__ __forceinline__ R S_at(const Ix<DIM, PER>& ix, R c0, int j, const int f[3], const FA& a, const FW& w) {
+  if (!PER && (f[j] == 0 || f[j] == ix.n(j))) return R(0);
+  R acc = R(0);
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    R ap, am;
+    int t[3];
+    if (k == j) {
+      // centre averages of a_j in the cells above / below the face
+      int up[3], dn[3];
+      shift((int*)f, j, 1, up);
+      shift((int*)f, j, -1, dn);
+      R aj = a(j, f[0], f[1], f[2]);
+      bool has_up = PER || f[j] < ix.n(j);
+      bool has_dn = PER || f[j] > 0;
+      ap = has_up ? R(0.5) * (aj + a(j, up[0], up[1], up[2])) : R(0);
+      am = has_dn ? R(0.5) * (a(j, dn[0], dn[1], dn[2]) + aj) : R(0);
+    } else {
+      // corners: a_k averaged along j at k-index f_k+1 (plus) / f_k (minus)
+      int p0[3], p1[3];
+      shift((int*)f, k, 1, p0);          // (f_j, f_k+1)
+      shift(p0, j, -1, p1);              // (f_j-1, f_k+1)
+      ap = R(0.5) * (a(k, p0[0], p0[1], p0[2]) + a(k, p1[0], p1[1], p1[2]));
+      shift((int*)f, j, -1, p1);         // (f_j-1, f_k)
+      am = R(0.5) * (a(k, f[0], f[1], f[2]) + a(k, p1[0], p1[1], p1[2]));
+    }
+    shift((int*)f, k, 1, t);
+    R wp = w(j, t[0], t[1], t[2]);
+    shift((int*)f, k, -1, t);
+    R wm = w(j, t[0], t[1], t[2]);
+    acc += ap * wp - am * wm;
+  }
+  return c0 * acc;
+}
+
+// ---------------------------------------------------------------------------
+// T(v, u)_k at one k-face g: adjoint of d -> S(d, v) tested against u
+// (advection.py:380-434).  J_Adv(v)^T u = T(v, u) - S(v, u) (advection.py:437).
+// ---------------------------------------------------------------------------
+template <int DIM, bool PER, class R, class FV, class FU>
+__device__ __forceinline__ R Tadj_at(const Ix<DIM, PER>& ix, R c0, int k, const int g[3], const FV& v, const FU& u) {
+  if (!PER && (g[k] == 0 || g[k] == ix.n(k))) return R(0);
+  R acc = R(0);
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    if (j == k) {
+      // gam[c] = c0 (u_k[c] v_k[c+e_k] - u_k[c+e_k] v_k[c]) on cells along k;
+      // out += 1/2 (gam[cell g] + gam[cell g - e_k])
+      R s = R(0);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        int c[3], cp[3];
+        shift((int*)g, k, -side, c);     // cell index (lower face of the cell) = c
+        if (!PER && (c[k] < 0 || c[k] >= ix.n(k))) continue;
+        shift(c, k, 1, cp);
+        s += u(k, c[0], c[1], c[2]) * v(k, cp[0], cp[1], cp[2]) - u(k, cp[0], cp[1], cp[2]) * v(k, c[0], c[1], c[2]);
+      }
+      acc += R(0.5) * c0 * s;
+    } else {
+      // gam_jk at (j-face index f_j, corner index f_k along k):
+      //   c0 (u_j[f - e_k] v_j[f] - u_j[f] v_j[f - e_k]),  interior f_k only;
+      // out_k[g] += 1/2 (gam[f_j = g_j] + gam[f_j = g_j + 1]) at f_k = g_k
+      if (!PER && (g[k] == 0 || g[k] == ix.n(k))) continue;
+      R s = R(0);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        int f[3], fm[3];
+        shift((int*)g, j, side, f);
+        shift(f, k, -1, fm);
+        s += u(j, fm[0], fm[1], fm[2]) * v(j, f[0], f[1], f[2]) - u(j, f[0], f[1], f[2]) * v(j, fm[0], fm[1], fm[2]);
+      }
+      acc += R(0.5) * c0 * s;
+    }
+  }
+  return acc;
+}
+
+template <int DIM, bool PER, class R, class FV, class FU>
+__device__ __forceinline__ R JT_at(const Ix<DIM, PER>& ix, R c0, int k, const int g[3], const FV& v, const FU& u) {
+  return Tadj_at<DIM, PER, R>(ix, c0, k, g, v, u) - S_at<DIM, PER, R>(ix, c0, k, g, v, u);
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+template <class R>
+__device__ __forceinline__ R warp_max(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <class R>
+__device__ __forceinline__ R warp_sum(R v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// atomic max of a non-negative value through its bit pattern (order-free,
+// hence deterministic)
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+__device__ __forceinline__ void atomic_max_nonneg(float* addr, float v) {
+  atomicMax((unsigned int*)addr, (unsigned int)__float_as_int(v));
+}
+
+template <class R>
+__device__ __forceinline__ void block_max_to(R v, R* out) {
+  __shared__ R sh[32];
+  v = warp_max(v);
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (lane < (int)(blockDim.x >> 5)) ? sh[lane] : R(0);
+    v = warp_max(v);
+    if (lane == 0 && v > R(0)) atomic_max_nonneg(out, v);
+  }
+}
+
+inline int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  const int64_t cap = 148 * 32;
+  return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
+}
+
+#define SMK_GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+}  // namespace smk

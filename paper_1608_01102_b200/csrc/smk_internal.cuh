@@ -1,0 +1,53 @@
+// Declarations shared between the translation units of libsmk.
+#pragma once
+
+#include <utility>
+#include <vector>
+
+#include "smk_dispatch.cuh"
+
+namespace smk {
+
+// device allocations released together (operator-level scratch)
+struct Scratch {
+  std::vector<std::pair<void*, size_t>> bufs;
+  void* get(size_t bytes);
+  void release();
+  ~Scratch();
+};
+
+Geo coarsen(const Geo& g);
+Geo refine(const Geo& g);
+bool can_coarsen(const Geo& g);
+int64_t cells_of(const Geo& g);
+int64_t faces_of(const Geo& g, int k);
+
+double host_absmax(int dtype, const void* x, int64_t n, cudaStream_t st, void* dev_scalar);
+double host_sum(int dtype, const void* x, const void* y, int64_t n, cudaStream_t st, double* dev_parts);
+template <class R>
+void frame_sub_mean(R* x, int64_t per, int nframes, cudaStream_t st, double* dev_parts);
+template <class R>
+void axpby(R* y, const R* x, double a, double b, int64_t n, cudaStream_t st);
+
+enum { OP_S = 0, OP_J = 1, OP_JT = 2 };
+
+// launch accounting (gpu_launches in bench.py): every kernel launch site of
+// the library calls count_launch()
+void count_launch(int n = 1);
+
+template <int DIM, bool PER, class R>
+void launch_div(const Geo& g, int N, Face3<R> v, R* out, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_grad(const Geo& g, int N, const R* p, FaceW<R> out, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_face_op(const Geo& g, int N, Face3<R> a, Face3<R> w, FaceW<R> out, int op, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_restrict_cell(const Geo& gf, int N, const R* x, R* out, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_prolong_cell(const Geo& gc, int N, const R* x, R* out, int acc, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_restrict_face(const Geo& gf, int N, Face3<R> in, FaceW<R> out, cudaStream_t st);
+template <int DIM, bool PER, class R>
+void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int acc, cudaStream_t st);
+
+}  // namespace smk

@@ -1,0 +1,1015 @@
+// STFAS / NSO: Eq. 8 KKT residual, coloured time-line SCGS smoother, FAS
+// V-cycle hierarchy (PAPER Eq. 8/9, Alg. 2).
+//
+// Semantics are frozen in DESIGN.md §3 and mirrored by oracle/stfas.py:
+//   pair index i = 0..N-1:  U[i]=u_i, P[i]=p_{i+1}, V[i]=v_{i+1}, PB[i]=pbar_{i+1}
+//   R3[i] = (v_{i+1}-v_i)/dt + Adv(v_{i+1}) - u_i + grad p_{i+1}
+//   R4[i] = div u_i
+//   R1[i] = [i<N-1]((K/r)(v_{i+1}-v*_{i+1}) - u_{i+1}/dt) + u_i/dt
+//           + J_Adv(v_{i+1})^T u_i + grad pbar_{i+1}
+//   R2[i] = div v_{i+1}
+// Smoother: per colour, every cell of the colour solves its 2N-block
+// (2d faces + 1 scalar) Gauss-Newton time line with the state frozen
+// (snapshot reads, writes go to a delta buffer), then the colour's unknowns
+// take x += omega * dx.  Same-colour cells own disjoint unknowns, so the
+// apply pass is race-free and the sweep is bitwise deterministic.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "smk_internal.cuh"
+
+namespace smk {
+
+template <class R>
+struct StP {
+  R* V[3];
+  R* PB;
+  R* U[3];
+  R* P;
+};
+template <class R>
+struct ResP {
+  R* R1[3];
+  R* R2;
+  R* R3[3];
+  R* R4;
+};
+
+struct NsoK {  // kernel-side scalars
+  int N;
+  double dt, kr, omega;
+};
+
+template <class R>
+__device__ __forceinline__ Face3<R> frame_of(const Face3<R>& base, int fr, const int64_t nf[3]) {
+  Face3<R> o;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) o.c[k] = base.c[k] ? base.c[k] + (int64_t)fr * nf[k] : nullptr;
+  return o;
+}
+
+// ---------------------------------------------------------------------------
+// point residuals (shared by the residual kernel and the smoother)
+// ---------------------------------------------------------------------------
+template <int DIM, bool PER, class R>
+struct KktCtx {
+  Ix<DIM, PER> ix;
+  R c0, h, dt, kr;
+  int N;
+  int64_t nf[3], nc;
+  Face3<R> V, U, v0, vs;
+  const R* P;
+  const R* PB;
+
+  __device__ __forceinline__ R grad_at(const R* p, int k, const int f[3]) const {
+    if (ix.wall(k, f)) return R(0);
+    int lo[3];
+    shift((int*)f, k, -1, lo);
+    return (ix.cell(p, f[0], f[1], f[2]) - ix.cell(p, lo[0], lo[1], lo[2])) / h;
+  }
+  __device__ __forceinline__ R div_at(const Face3<R>& v, const int c[3]) const {
+    R acc = R(0);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      int hi[3];
+      shift((int*)c, k, 1, hi);
+      R d = (ix.face(v.c[k], k, hi[0], hi[1], hi[2]) - v.c[k][ix.face_off(k, c[0], c[1], c[2])]) / h;
+      acc = (k == 0) ? d : acc + d;
+    }
+    return acc;
+  }
+  // R3[i] at j-face f
+  __device__ R r3(int i, int j, const int f[3]) const {
+    if (ix.wall(j, f)) return R(0);
+    Face3<R> Vi = frame_of(V, i, nf);
+    Face3<R> Vp = i == 0 ? v0 : frame_of(V, i - 1, nf);
+    int64_t o = ix.face_off(j, f[0], f[1], f[2]);
+    MemField<DIM, PER, R> A{ix, Vi};
+    R adv = S_at<DIM, PER, R>(ix, c0, j, f, A, A);
+    R u = U.c[j][(int64_t)i * nf[j] + o];
+    R q = grad_at(P + (int64_t)i * nc, j, f);
+    return (((Vi.c[j][o] - Vp.c[j][o]) / dt + adv) - u) + q;
+  }
+  // R1[i] at j-face f
+  __device__ R r1(int i, int j, const int f[3]) const {
+    if (ix.wall(j, f)) return R(0);
+    Face3<R> Vi = frame_of(V, i, nf);
+    Face3<R> Ui = frame_of(U, i, nf);
+    int64_t o = ix.face_off(j, f[0], f[1], f[2]);
+    R t1 = R(0);
+    if (i < N - 1) {
+      R s = vs.c[j][(int64_t)(i + 1) * nf[j] + o];
+      R un = U.c[j][(int64_t)(i + 1) * nf[j] + o];
+      t1 = kr * (Vi.c[j][o] - s) - un / dt;
+    }
+    MemField<DIM, PER, R> Av{ix, Vi}, Au{ix, Ui};
+    R jt = JT_at<DIM, PER, R>(ix, c0, j, f, Av, Au);
+    R q = grad_at(PB + (int64_t)i * nc, j, f);
+    return ((t1 + Ui.c[j][o] / dt) + jt) + q;
+  }
+  __device__ R r2(int i, const int c[3]) const { return div_at(frame_of(V, i, nf), c); }
+  __device__ R r4(int i, const int c[3]) const { return div_at(frame_of(U, i, nf), c); }
+};
+
+template <int DIM, bool PER, class R>
+__global__ void k_kkt_faces(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
+  const int j = blockIdx.y;
+  const int64_t nf = cx.nf[j];
+  SMK_GRID_STRIDE(t, (int64_t)cx.N * nf) {
+    int i = (int)(t / nf);
+    int f[3];
+    cx.ix.face_idx(j, t - (int64_t)i * nf, f);
+    R a = cx.r1(i, j, f), b = cx.r3(i, j, f);
+    if (has_rhs) {
+      a -= rhs.R1[j][t];
+      b -= rhs.R3[j][t];
+    }
+    out.R1[j][t] = a;
+    out.R3[j][t] = b;
+  }
+}
+
+template <int DIM, bool PER, class R>
+__global__ void k_kkt_cells(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
+  const int64_t nc = cx.nc;
+  SMK_GRID_STRIDE(t, (int64_t)cx.N * nc) {
+    int i = (int)(t / nc);
+    int c[3];
+    cx.ix.cell_idx(t - (int64_t)i * nc, c);
+    R a = cx.r2(i, c), b = cx.r4(i, c);
+    if (has_rhs) {
+      a -= rhs.R2[t];
+      b -= rhs.R4[t];
+    }
+    out.R2[t] = a;
+    out.R4[t] = b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the time-line SCGS smoother
+// ---------------------------------------------------------------------------
+
+// Dense solve S [W | z] = [RHS], B x B with C right-hand sides, in registers.
+// PIVOT selects partial pivoting (tournament row swaps, fully unrolled so the
+// arrays stay in registers); definite blocks use the natural order.
+template <class R, int B, int C, bool PIVOT>
+__device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) {
+  bool ok = true;
+#pragma unroll
+  for (int col = 0; col < B; ++col) {
+    if (PIVOT) {
+#pragma unroll
+      for (int r = col + 1; r < B; ++r) {
+        bool sw = abs(A[r][col]) > abs(A[col][col]);
+#pragma unroll
+        for (int c = 0; c < B; ++c) {
+          R a = A[col][c], b = A[r][c];
+          A[col][c] = sw ? b : a;
+          A[r][c] = sw ? a : b;
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+          R a = X[col][c], b = X[r][c];
+          X[col][c] = sw ? b : a;
+          X[r][c] = sw ? a : b;
+        }
+      }
+    }
+    R piv = A[col][col];
+    if (!(abs(piv) > tiny)) ok = false;
+    R inv = R(1) / piv;
+#pragma unroll
+    for (int r = col + 1; r < B; ++r) {
+      R fct = A[r][col] * inv;
+#pragma unroll
+      for (int c = col + 1; c < B; ++c) A[r][c] -= fct * A[col][c];
+#pragma unroll
+      for (int c = 0; c < C; ++c) X[r][c] -= fct * X[col][c];
+    }
+  }
+#pragma unroll
+  for (int r = B - 1; r >= 0; --r) {
+    R inv = R(1) / A[r][r];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      R s = X[r][c];
+#pragma unroll
+      for (int q = r + 1; q < B; ++q) s -= A[r][q] * X[q][c];
+      X[r][c] = s * inv;
+    }
+  }
+  return ok;
+}
+
+template <int DIM>
+struct Slots {
+  static constexpr int NF = 2 * DIM;
+  static constexpr int B = NF + 1;
+  static constexpr int C = NF + 1;  // W columns (faces) + z
+};
+
+// scratch layout: [block][entry][m] with entry = row * C + col
+template <int DIM, bool PER, class R>
+__global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1,
+                                                   int o2, int mod, int m0, int m1, int m2, R omega,
+                                                   R* __restrict__ scratch, R* __restrict__ xout, int* flag) {
+  constexpr int NF = Slots<DIM>::NF, B = Slots<DIM>::B, C = Slots<DIM>::C;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const auto& ix = cx.ix;
+  int c[3];
+  {
+    int64_t q = m;
+    int q2 = (int)(q % m2); q /= m2;
+    int q1 = (int)(q % m1); q /= m1;
+    c[0] = o0 + mod * (int)q;
+    c[1] = o1 + mod * q1;
+    c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+  }
+  // local face slots q = 2k + s
+  int fidx[NF][3];
+  bool wall[NF];
+  R gcol[NF];
+#pragma unroll
+  for (int k = 0; k < DIM; ++k)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      int q = 2 * k + s;
+      fidx[q][0] = c[0]; fidx[q][1] = c[1]; fidx[q][2] = c[2];
+      fidx[q][k] += s;
+      if (PER && fidx[q][k] >= ix.n(k)) fidx[q][k] -= ix.n(k);
+      wall[q] = !PER && (s == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
+      gcol[q] = wall[q] ? R(0) : (s == 0 ? R(1) : R(-1)) / cx.h;
+    }
+  const R idt = R(1) / cx.dt;
+  const int N = cx.N;
+  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+  bool ok = true;
+  R zprev[B];    // z of the previous block
+  R Wprev[B][NF];  // W of the previous block (face columns)
+#pragma unroll
+  for (int a = 0; a < B; ++a) {
+    zprev[a] = R(0);
+#pragma unroll
+    for (int b = 0; b < NF; ++b) Wprev[a][b] = R(0);
+  }
+  auto store = [&](int blk, R (&X)[B][C]) {
+    R* base = scratch + (int64_t)blk * B * C * M + m;
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int q = 0; q < C; ++q) base[(int64_t)(r * C + q) * M] = X[r][q];
+  };
+
+  for (int i = 0; i < N; ++i) {
+    // ---- local Jacobian of Adv at v_{i+1} on the cell's faces ----
+    R J[NF][NF];
+    {
+      Face3<R> Vi = frame_of(cx.V, i, cx.nf);
+      MemField<DIM, PER, R> Av{ix, Vi};
+#pragma unroll
+      for (int qc = 0; qc < NF; ++qc) {
+        UnitField<DIM, PER, R> E{ix, qc >> 1, fidx[qc][0], fidx[qc][1], fidx[qc][2]};
+#pragma unroll
+        for (int qr = 0; qr < NF; ++qr) {
+          R v = R(0);
+          if (!wall[qr] && !wall[qc])
+            v = S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, fidx[qr], Av, E) +
+                S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, fidx[qr], E, Av);
+          J[qr][qc] = v;
+        }
+      }
+    }
+    // ================= u-block (rows R3[i], R4[i]; unknowns u_i, p_{i+1}) =====
+    {
+      R A[B][B], X[B][C];
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) A[r][q] = R(0);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        A[q][q] = wall[q] ? R(1) : R(-1);
+        A[q][NF] = gcol[q];
+        A[NF][q] = -gcol[q];
+      }
+      // rhs = -(f - rhs)
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        R y = R(0);
+        if (!wall[q]) {
+          int j = q >> 1;
+          y = cx.r3(i, j, fidx[q]);
+          if (has_rhs) y -= rhs.R3[j][(int64_t)i * cx.nf[j] + ix.face_off(j, fidx[q][0], fidx[q][1], fidx[q][2])];
+        }
+        X[q][NF] = -y;
+      }
+      {
+        R y = cx.r4(i, c);
+        if (has_rhs) y -= rhs.R4[(int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2])];
+        X[NF][NF] = -y;
+      }
+      // coupling to the previous v-block (v_i): L = -I/dt on faces
+      if (i > 0) {
+#pragma unroll
+        for (int r = 0; r < NF; ++r) {
+          if (wall[r]) continue;
+#pragma unroll
+          for (int q = 0; q < NF; ++q) A[r][q] += idt * Wprev[r][q];
+          X[r][NF] += idt * zprev[r];
+        }
+      }
+      // upper coupling to v_{i+1}: I/dt + J
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < NF; ++q) X[r][q] = (r < NF) ? (J[r][q] + ((r == q && !wall[q]) ? idt : R(0))) : R(0);
+      ok &= dense_solve<R, B, C, false>(A, X, tinyv);
+      store(2 * i, X);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        zprev[r] = X[r][NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
+      }
+    }
+    // ================= v-block (rows R1[i], R2[i]; unknowns v_{i+1}, pbar) ====
+    {
+      R A[B][B], X[B][C];
+      const R alpha = (i < N - 1) ? cx.kr : R(0);
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < B; ++q) A[r][q] = R(0);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        A[q][q] = wall[q] ? R(1) : alpha;
+        A[q][NF] = gcol[q];
+        A[NF][q] = -gcol[q];
+      }
+#pragma unroll
+      for (int q = 0; q < NF; ++q) {
+        R y = R(0);
+        if (!wall[q]) {
+          int j = q >> 1;
+          y = cx.r1(i, j, fidx[q]);
+          if (has_rhs) y -= rhs.R1[j][(int64_t)i * cx.nf[j] + ix.face_off(j, fidx[q][0], fidx[q][1], fidx[q][2])];
+        }
+        X[q][NF] = -y;
+      }
+      {
+        R y = cx.r2(i, c);
+        if (has_rhs) y -= rhs.R2[(int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2])];
+        X[NF][NF] = -y;
+      }
+      // lower coupling to u_i: L = I/dt + J^T  ->  A -= L Wprev, rhs -= L zprev
+#pragma unroll
+      for (int r = 0; r < NF; ++r) {
+        if (wall[r]) continue;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) {
+          R s = R(0);
+#pragma unroll
+          for (int t = 0; t < NF; ++t) {
+            R L = J[t][r] + ((t == r && !wall[r]) ? idt : R(0));
+            s += L * Wprev[t][q];
+          }
+          A[r][q] -= s;
+        }
+        R s = R(0);
+#pragma unroll
+        for (int t = 0; t < NF; ++t) {
+          R L = J[t][r] + ((t == r && !wall[r]) ? idt : R(0));
+          s += L * zprev[t];
+        }
+        X[r][NF] -= s;
+      }
+      // upper coupling to u_{i+1}: -I/dt
+#pragma unroll
+      for (int r = 0; r < B; ++r)
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+          X[r][q] = (i < N - 1 && r < NF && r == q && !wall[q]) ? -idt : R(0);
+      if (i < N - 1) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
+      else ok &= dense_solve<R, B, C, true>(A, X, tinyv);
+      store(2 * i + 1, X);
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        zprev[r] = X[r][NF];
+#pragma unroll
+        for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
+      }
+    }
+  }
+  // ---- back substitution: x_b = z_b - W_b x_{b+1}[faces] ----
+  R xn[NF];
+#pragma unroll
+  for (int q = 0; q < NF; ++q) xn[q] = R(0);
+  for (int blk = 2 * N - 1; blk >= 0; --blk) {
+    const R* base = scratch + (int64_t)blk * B * C * M + m;
+    R xb[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      R s = base[(int64_t)(r * C + NF) * M];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) s -= base[(int64_t)(r * C + q) * M] * xn[q];
+      xb[r] = s;
+    }
+    R* xo = xout + (int64_t)blk * B * M + m;
+#pragma unroll
+    for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
+#pragma unroll
+    for (int q = 0; q < NF; ++q) xn[q] = xb[q];
+  }
+  if (!ok) atomicExch(flag, 1);
+}
+
+// x += omega * dx on the colour's unknowns (disjoint across cells)
+template <int DIM, bool PER, class R>
+__global__ void k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, int N, int o0, int o1, int o2, int mod, int m0, int m1, int m2,
+                             const R* __restrict__ xout) {
+  constexpr int NF = 2 * DIM, B = NF + 1;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  int64_t nf[3] = {ix.faces(0), ix.faces(1), DIM == 3 ? ix.faces(2) : 0};
+  SMK_GRID_STRIDE(t, (int64_t)N * M) {
+    int i = (int)(t / M);
+    int64_t m = t - (int64_t)i * M;
+    int c[3];
+    int64_t q = m;
+    int q2 = (int)(q % m2); q /= m2;
+    int q1 = (int)(q % m1); q /= m1;
+    c[0] = o0 + mod * (int)q;
+    c[1] = o1 + mod * q1;
+    c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+    const R* xu = xout + (int64_t)(2 * i) * B * M + m;
+    const R* xv = xout + (int64_t)(2 * i + 1) * B * M + m;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd) {
+        int qq = 2 * k + sd;
+        bool w = !PER && (sd == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
+        if (w) continue;
+        int f[3] = {c[0], c[1], c[2]};
+        f[k] += sd;
+        if (PER && f[k] >= ix.n(k)) f[k] -= ix.n(k);
+        int64_t o = (int64_t)i * nf[k] + ix.face_off(k, f[0], f[1], f[2]);
+        s.U[k][o] += xu[(int64_t)qq * M];
+        s.V[k][o] += xv[(int64_t)qq * M];
+      }
+    int64_t oc = (int64_t)i * ix.cells() + ix.cell_off(c[0], c[1], c[2]);
+    s.P[oc] += xu[(int64_t)NF * M];
+    s.PB[oc] += xv[(int64_t)NF * M];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host: hierarchy
+// ---------------------------------------------------------------------------
+template <class R>
+struct Level {
+  Geo g;
+  StP<R> st{};      // state (levels >= 1 owned; level 0 bound per call)
+  StP<R> st0{};     // restricted copy (coarse levels)
+  ResP<R> rhs{};    // FAS rhs (levels >= 1)
+  ResP<R> f{};      // residual buffer
+  R* v0[3] = {nullptr, nullptr, nullptr};
+  R* vs[3] = {nullptr, nullptr, nullptr};
+  int64_t nc = 0, nf[3] = {0, 0, 0};
+};
+
+struct NsoBase {
+  virtual ~NsoBase() {}
+  virtual int set_guide(const void* const v0[], const void* const vstar[], cudaStream_t st) = 0;
+  virtual int vcycle(const smk_state* s, cudaStream_t st) = 0;
+  virtual int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) = 0;
+  virtual int gauge(const smk_state* s, cudaStream_t st) = 0;
+  virtual int levels() const = 0;
+  virtual int profile(int enable) = 0;
+  virtual int profile_read(double* ms, long long* launches, long long* cells) = 0;
+  virtual int64_t bytes() const = 0;
+};
+
+template <int DIM, bool PER, class R>
+struct Nso : NsoBase {
+  smk_nso_params prm;
+  std::vector<Level<R>> lv;
+  Scratch mem;
+  int64_t nbytes = 0;
+  R* scratch = nullptr;   // smoother W/z
+  R* xout = nullptr;      // smoother deltas
+  int* flag = nullptr;
+  double* parts = nullptr;
+  void* scal = nullptr;
+  bool ok = true;
+  const void* top_v0[3] = {nullptr, nullptr, nullptr};
+  const void* top_vs[3] = {nullptr, nullptr, nullptr};
+  bool guide_set = false;
+  // optional CUDA-event profile of the smoother's colour kernel
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t ev_used = 0;
+  int64_t prof_cells = 0;  // cell-timesteps processed by profiled launches
+
+  R* alloc(int64_t n) {
+    void* p = mem.get((size_t)n * sizeof(R));
+    if (!p) ok = false;
+    else cudaMemset(p, 0, (size_t)n * sizeof(R));
+    nbytes += n * (int64_t)sizeof(R);
+    return (R*)p;
+  }
+
+  Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
+    int want = p.n_levels < 1 ? 1 : p.n_levels;
+    Geo cur = g;
+    for (int l = 0; l < want; ++l) {
+      Level<R> L;
+      L.g = cur;
+      L.nc = cells_of(cur);
+      for (int k = 0; k < DIM; ++k) L.nf[k] = faces_of(cur, k);
+      lv.push_back(L);
+      if (!can_coarsen(cur)) break;
+      cur = coarsen(cur);
+    }
+    const int N = p.n_frames;
+    int64_t maxM = 0;
+    for (size_t l = 0; l < lv.size(); ++l) {
+      Level<R>& L = lv[l];
+      auto face_alloc = [&](R* (&dst)[3], int frames) {
+        for (int k = 0; k < 3; ++k) dst[k] = k < DIM ? alloc((int64_t)frames * L.nf[k]) : nullptr;
+      };
+      if (l > 0) {
+        face_alloc(L.st.V, N); L.st.PB = alloc((int64_t)N * L.nc);
+        face_alloc(L.st.U, N); L.st.P = alloc((int64_t)N * L.nc);
+        face_alloc(L.st0.V, N); L.st0.PB = alloc((int64_t)N * L.nc);
+        face_alloc(L.st0.U, N); L.st0.P = alloc((int64_t)N * L.nc);
+        face_alloc(L.rhs.R1, N); L.rhs.R2 = alloc((int64_t)N * L.nc);
+        face_alloc(L.rhs.R3, N); L.rhs.R4 = alloc((int64_t)N * L.nc);
+        face_alloc(L.v0, 1);
+        face_alloc(L.vs, N);
+      }
+      face_alloc(L.f.R1, N); L.f.R2 = alloc((int64_t)N * L.nc);
+      face_alloc(L.f.R3, N); L.f.R4 = alloc((int64_t)N * L.nc);
+      int64_t M = 1;
+      for (int a = 0; a < DIM; ++a) M *= (L.g.n[a] + p.color_mod - 1) / p.color_mod;
+      maxM = M > maxM ? M : maxM;
+    }
+    constexpr int B = Slots<DIM>::B, C = Slots<DIM>::C;
+    scratch = alloc((int64_t)2 * N * B * C * maxM);
+    xout = alloc((int64_t)2 * N * B * maxM);
+    flag = (int*)mem.get(64);
+    parts = (double*)mem.get(sizeof(double) * 70000);
+    scal = mem.get(64);
+    if (!flag || !parts || !scal) ok = false;
+  }
+
+  int levels() const override { return (int)lv.size(); }
+  int profile(int enable) override {
+    prof = enable != 0;
+    ev_used = 0;
+    prof_cells = 0;
+    return SMK_OK;
+  }
+  int profile_read(double* ms, long long* launches, long long* cells) override {
+    double tot = 0.0;
+    for (size_t i = 0; i < ev_used; ++i) {
+      cudaEventSynchronize(ev[i].second);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[i].first, ev[i].second);
+      tot += t;
+    }
+    if (ms) *ms = tot;
+    if (launches) *launches = (long long)ev_used;
+    if (cells) *cells = (long long)prof_cells;
+    return cuda_check("nso_profile_read");
+  }
+  ~Nso() override {
+    for (auto& e : ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  }
+  int64_t bytes() const override { return nbytes; }
+
+  KktCtx<DIM, PER, R> ctx(int l, const StP<R>& s) const {
+    const Level<R>& L = lv[l];
+    KktCtx<DIM, PER, R> c{Ix<DIM, PER>(L.g)};
+    c.c0 = (R)(0.5 / L.g.h);
+    c.h = (R)L.g.h;
+    c.dt = (R)prm.dt;
+    c.kr = (R)(prm.K / prm.r);
+    c.N = prm.n_frames;
+    for (int k = 0; k < 3; ++k) c.nf[k] = L.nf[k];
+    c.nc = L.nc;
+    for (int k = 0; k < 3; ++k) {
+      c.V.c[k] = s.V[k];
+      c.U.c[k] = s.U[k];
+      c.v0.c[k] = l == 0 ? (const R*)top_v0[k] : L.v0[k];
+      c.vs.c[k] = l == 0 ? (const R*)top_vs[k] : L.vs[k];
+    }
+    c.P = s.P;
+    c.PB = s.PB;
+    return c;
+  }
+
+  static StP<R> from_api(const smk_state* s) {
+    StP<R> o;
+    for (int k = 0; k < 3; ++k) {
+      o.V[k] = (R*)s->V[k];
+      o.U[k] = (R*)s->U[k];
+    }
+    o.PB = (R*)s->PB;
+    o.P = (R*)s->P;
+    return o;
+  }
+
+  void residual(int l, const StP<R>& s, const ResP<R>* rhs, const ResP<R>& out, cudaStream_t st) {
+    auto c = ctx(l, s);
+    int64_t nfa = (int64_t)prm.n_frames * lv[l].nf[0];
+    dim3 gf(grid_for(nfa, 128), DIM);
+    ResP<R> r = rhs ? *rhs : ResP<R>{};
+    k_kkt_faces<DIM, PER, R><<<gf, 128, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
+    int64_t nca = (int64_t)prm.n_frames * lv[l].nc;
+    k_kkt_cells<DIM, PER, R><<<grid_for(nca, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
+  }
+
+  void sweep(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
+    const Level<R>& L = lv[l];
+    const int mod = prm.color_mod;
+    int ncol = 1;
+    for (int a = 0; a < DIM; ++a) ncol *= mod;
+    auto c = ctx(l, s);
+    ResP<R> r = rhs ? *rhs : ResP<R>{};
+    Ix<DIM, PER> ix(L.g);
+    for (int col = 0; col < ncol; ++col) {
+      int o[3] = {0, 0, 0}, mm[3] = {1, 1, 1};
+      int cc = col;
+      for (int a = 0; a < DIM; ++a) {
+        o[a] = cc % mod;
+        cc /= mod;
+        mm[a] = (L.g.n[a] - o[a] + mod - 1) / mod;
+        if (mm[a] < 0) mm[a] = 0;
+      }
+      int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
+      if (M == 0) continue;
+      cudaEvent_t e1 = nullptr, e2 = nullptr;
+      if (prof) {
+        if (ev_used == ev.size()) {
+          cudaEvent_t a, b;
+          cudaEventCreate(&a);
+          cudaEventCreate(&b);
+          ev.push_back({a, b});
+        }
+        e1 = ev[ev_used].first;
+        e2 = ev[ev_used].second;
+        ++ev_used;
+        prof_cells += M * prm.n_frames;
+        cudaEventRecord(e1, st);
+      }
+      k_scgs_color<DIM, PER, R><<<(unsigned)((M + 127) / 128), 128, 0, st>>>(
+          c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout, flag); count_launch();
+      if (prof) cudaEventRecord(e2, st);
+      int64_t tot = (int64_t)prm.n_frames * M;
+      k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
+                                                                     mm[1], mm[2], xout); count_launch();
+    }
+  }
+
+  void restrict_state(int l, const StP<R>& fine, const StP<R>& coarse, cudaStream_t st) {
+    const int N = prm.n_frames;
+    Face3<R> a, b;
+    FaceW<R> oa, ob;
+    for (int k = 0; k < 3; ++k) {
+      a.c[k] = fine.V[k]; b.c[k] = fine.U[k];
+      oa.c[k] = coarse.V[k]; ob.c[k] = coarse.U[k];
+    }
+    launch_restrict_face<DIM, PER, R>(lv[l].g, N, a, oa, st);
+    launch_restrict_face<DIM, PER, R>(lv[l].g, N, b, ob, st);
+    launch_restrict_cell<DIM, PER, R>(lv[l].g, N, fine.PB, coarse.PB, st);
+    launch_restrict_cell<DIM, PER, R>(lv[l].g, N, fine.P, coarse.P, st);
+  }
+
+  void restrict_res(int l, const ResP<R>& fine, const ResP<R>& coarse, cudaStream_t st) {
+    const int N = prm.n_frames;
+    Face3<R> a, b;
+    FaceW<R> oa, ob;
+    for (int k = 0; k < 3; ++k) {
+      a.c[k] = fine.R1[k]; b.c[k] = fine.R3[k];
+      oa.c[k] = coarse.R1[k]; ob.c[k] = coarse.R3[k];
+    }
+    launch_restrict_face<DIM, PER, R>(lv[l].g, N, a, oa, st);
+    launch_restrict_face<DIM, PER, R>(lv[l].g, N, b, ob, st);
+    launch_restrict_cell<DIM, PER, R>(lv[l].g, N, fine.R2, coarse.R2, st);
+    launch_restrict_cell<DIM, PER, R>(lv[l].g, N, fine.R4, coarse.R4, st);
+  }
+
+  void copy_state(int l, const StP<R>& src, const StP<R>& dst, cudaStream_t st) {
+    const int N = prm.n_frames;
+    const Level<R>& L = lv[l];
+    for (int k = 0; k < DIM; ++k) {
+      cudaMemcpyAsync(dst.V[k], src.V[k], (size_t)N * L.nf[k] * sizeof(R), cudaMemcpyDeviceToDevice, st);
+      cudaMemcpyAsync(dst.U[k], src.U[k], (size_t)N * L.nf[k] * sizeof(R), cudaMemcpyDeviceToDevice, st);
+    }
+    cudaMemcpyAsync(dst.PB, src.PB, (size_t)N * L.nc * sizeof(R), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(dst.P, src.P, (size_t)N * L.nc * sizeof(R), cudaMemcpyDeviceToDevice, st);
+  }
+
+  // dst = a*src + b*dst over the whole state
+  void axpby_state(int l, const StP<R>& src, const StP<R>& dst, double a, double b, cudaStream_t st) {
+    const int N = prm.n_frames;
+    const Level<R>& L = lv[l];
+    for (int k = 0; k < DIM; ++k) {
+      axpby<R>(dst.V[k], src.V[k], a, b, (int64_t)N * L.nf[k], st);
+      axpby<R>(dst.U[k], src.U[k], a, b, (int64_t)N * L.nf[k], st);
+    }
+    axpby<R>(dst.PB, src.PB, a, b, (int64_t)N * L.nc, st);
+    axpby<R>(dst.P, src.P, a, b, (int64_t)N * L.nc, st);
+  }
+
+  void prolong_add(int lc, const StP<R>& coarse, const StP<R>& fine, cudaStream_t st) {
+    const int N = prm.n_frames;
+    Face3<R> a, b;
+    FaceW<R> oa, ob;
+    for (int k = 0; k < 3; ++k) {
+      a.c[k] = coarse.V[k]; b.c[k] = coarse.U[k];
+      oa.c[k] = fine.V[k]; ob.c[k] = fine.U[k];
+    }
+    launch_prolong_face<DIM, PER, R>(lv[lc].g, N, a, oa, 1, st);
+    launch_prolong_face<DIM, PER, R>(lv[lc].g, N, b, ob, 1, st);
+    launch_prolong_cell<DIM, PER, R>(lv[lc].g, N, coarse.PB, fine.PB, 1, st);
+    launch_prolong_cell<DIM, PER, R>(lv[lc].g, N, coarse.P, fine.P, 1, st);
+  }
+
+  int set_guide(const void* const v0[], const void* const vstar[], cudaStream_t st) override {
+    for (int k = 0; k < 3; ++k) {
+      top_v0[k] = k < DIM ? v0[k] : nullptr;
+      top_vs[k] = k < DIM ? vstar[k] : nullptr;
+    }
+    for (size_t l = 1; l < lv.size(); ++l) {
+      Face3<R> a, b;
+      FaceW<R> oa, ob;
+      for (int k = 0; k < 3; ++k) {
+        a.c[k] = l == 1 ? (const R*)top_v0[k] : lv[l - 1].v0[k];
+        b.c[k] = l == 1 ? (const R*)top_vs[k] : lv[l - 1].vs[k];
+        oa.c[k] = lv[l].v0[k];
+        ob.c[k] = lv[l].vs[k];
+      }
+      launch_restrict_face<DIM, PER, R>(lv[l - 1].g, 1, a, oa, st);
+      launch_restrict_face<DIM, PER, R>(lv[l - 1].g, prm.n_frames, b, ob, st);
+    }
+    guide_set = true;
+    return cuda_check("nso_set_guide");
+  }
+
+  void vcycle_level(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
+    if (l == (int)lv.size() - 1) {
+      for (int it = 0; it < prm.n_coarse; ++it) sweep(l, s, rhs, st);
+      return;
+    }
+    for (int it = 0; it < prm.nu1; ++it) sweep(l, s, rhs, st);
+    Level<R>& C = lv[l + 1];
+    restrict_state(l, s, C.st, st);
+    copy_state(l + 1, C.st, C.st0, st);
+    // f = f(x) - rhs on this level; coarse rhs = f_c(R x) - R f
+    residual(l, s, rhs, lv[l].f, st);
+    restrict_res(l, lv[l].f, C.f, st);
+    residual(l + 1, C.st, &C.f, C.rhs, st);
+    vcycle_level(l + 1, C.st, &C.rhs, st);
+    // x += P(x_c - R x)
+    axpby_state(l + 1, C.st, C.st0, 1.0, -1.0, st);
+    prolong_add(l + 1, C.st0, s, st);
+    for (int it = 0; it < prm.nu2; ++it) sweep(l, s, rhs, st);
+  }
+
+  int check_flag(cudaStream_t st) {
+    int h = 0;
+    cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int rc = cuda_check("nso");
+    if (rc) return rc;
+    if (h) {
+      cudaMemsetAsync(flag, 0, sizeof(int), st);
+      set_error("SCGS block pivot below threshold (SingularBlock)");
+      return SMK_SINGULAR_BLOCK;
+    }
+    return SMK_OK;
+  }
+
+  int vcycle(const smk_state* s, cudaStream_t st) override {
+    if (!guide_set) { set_error("nso: set_guide not called"); return SMK_ERR_ARG; }
+    StP<R> top = from_api(s);
+    vcycle_level(0, top, nullptr, st);
+    return cuda_check("nso_vcycle");
+  }
+
+  int gauge(const smk_state* s, cudaStream_t st) override {
+    StP<R> top = from_api(s);
+    frame_sub_mean<R>(top.P, lv[0].nc, prm.n_frames, st, parts);
+    frame_sub_mean<R>(top.PB, lv[0].nc, prm.n_frames, st, parts);
+    return cuda_check("nso_gauge");
+  }
+
+  int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) override {
+    if (!guide_set) { set_error("nso: set_guide not called"); return SMK_ERR_ARG; }
+    StP<R> top = from_api(s);
+    const Level<R>& L = lv[0];
+    residual(0, top, nullptr, L.f, st);
+    const int N = prm.n_frames;
+    int dt = sizeof(R) == 8 ? SMK_F64 : SMK_F32;
+    double m = 0.0, q = 0.0;
+    for (int k = 0; k < DIM; ++k) {
+      m = std::max(m, host_absmax(dt, L.f.R1[k], (int64_t)N * L.nf[k], st, scal));
+      m = std::max(m, host_absmax(dt, L.f.R3[k], (int64_t)N * L.nf[k], st, scal));
+      if (r2) {
+        q += host_sum(dt, L.f.R1[k], L.f.R1[k], (int64_t)N * L.nf[k], st, parts);
+        q += host_sum(dt, L.f.R3[k], L.f.R3[k], (int64_t)N * L.nf[k], st, parts);
+      }
+    }
+    m = std::max(m, host_absmax(dt, L.f.R2, (int64_t)N * L.nc, st, scal));
+    m = std::max(m, host_absmax(dt, L.f.R4, (int64_t)N * L.nc, st, scal));
+    if (r2) {
+      q += host_sum(dt, L.f.R2, L.f.R2, (int64_t)N * L.nc, st, parts);
+      q += host_sum(dt, L.f.R4, L.f.R4, (int64_t)N * L.nc, st, parts);
+      *r2 = std::sqrt(q);
+    }
+    *ri = m;
+    return check_flag(st);
+  }
+
+  // standalone entry points (level-0 only)
+  int residual_api(const smk_state* s, const smk_residual* rhs, const smk_residual* out, cudaStream_t st) {
+    StP<R> top = from_api(s);
+    ResP<R> o, r;
+    for (int k = 0; k < 3; ++k) {
+      o.R1[k] = (R*)out->R1[k]; o.R3[k] = (R*)out->R3[k];
+      if (rhs) { r.R1[k] = (R*)rhs->R1[k]; r.R3[k] = (R*)rhs->R3[k]; }
+    }
+    o.R2 = (R*)out->R2; o.R4 = (R*)out->R4;
+    if (rhs) { r.R2 = (R*)rhs->R2; r.R4 = (R*)rhs->R4; }
+    residual(0, top, rhs ? &r : nullptr, o, st);
+    return cuda_check("smk_kkt_residual");
+  }
+  int sweep_api(const smk_state* s, const smk_residual* rhs, cudaStream_t st) {
+    StP<R> top = from_api(s);
+    ResP<R> r;
+    if (rhs) {
+      for (int k = 0; k < 3; ++k) { r.R1[k] = (R*)rhs->R1[k]; r.R3[k] = (R*)rhs->R3[k]; }
+      r.R2 = (R*)rhs->R2; r.R4 = (R*)rhs->R4;
+    }
+    sweep(0, top, rhs ? &r : nullptr, st);
+    return check_flag(st);
+  }
+};
+
+}  // namespace smk
+
+using namespace smk;
+
+struct smk_nso {
+  NsoBase* impl;
+  smk_grid grid;
+  smk_nso_params prm;
+};
+
+static int check_params(const smk_nso_params* p) {
+  if (!p) { set_error("null params"); return SMK_ERR_ARG; }
+  if (p->n_frames < 1) { set_error("n_frames must be >= 1"); return SMK_ERR_ARG; }
+  if (!(p->dt > 0) || !(p->r > 0) || !(p->K >= 0)) { set_error("dt, r must be positive, K >= 0"); return SMK_ERR_ARG; }
+  if (p->color_mod < 2) { set_error("color_mod must be >= 2"); return SMK_ERR_ARG; }
+  if (p->nu1 < 0 || p->nu2 < 0 || p->n_coarse < 0) { set_error("negative sweep counts"); return SMK_ERR_ARG; }
+  return SMK_OK;
+}
+
+template <class F>
+static NsoBase* make_nso(const smk_grid* g, const smk_nso_params* p) {
+  NsoBase* out = nullptr;
+  dispatch(g, [&](auto tag) {
+    using T = decltype(tag);
+    auto* n = new Nso<T::DIM, T::PER, typename T::R>(to_geo(g), *p);
+    if (!n->ok) {
+      delete n;
+      set_error("nso: device allocation failed");
+      return SMK_ERR_CUDA;
+    }
+    out = n;
+    return SMK_OK;
+  });
+  return out;
+}
+
+extern "C" {
+
+smk_nso* smk_nso_create(const smk_grid* g, const smk_nso_params* p) {
+  if (check_grid(g) || check_params(p)) return nullptr;
+  NsoBase* impl = make_nso<int>(g, p);
+  if (!impl) return nullptr;
+  smk_nso* h = new smk_nso;
+  h->impl = impl;
+  h->grid = *g;
+  h->prm = *p;
+  return h;
+}
+
+void smk_nso_destroy(smk_nso* h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  delete h->impl;
+  delete h;
+}
+
+int smk_nso_levels(const smk_nso* h) { return h ? h->impl->levels() : 0; }
+
+int smk_nso_profile(smk_nso* h, int enable) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->profile(enable);
+}
+
+int smk_nso_profile_read(smk_nso* h, double* ms, long long* launches, long long* cells) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->profile_read(ms, launches, cells);
+}
+int64_t smk_nso_device_bytes(const smk_nso* h) { return h ? h->impl->bytes() : 0; }
+
+int smk_nso_set_guide(smk_nso* h, const void* const v0[], const void* const vstar[], void* stream) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->set_guide(v0, vstar, (cudaStream_t)stream);
+}
+
+int smk_nso_vcycle(smk_nso* h, const smk_state* s, void* stream) {
+  if (!h || !s) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->vcycle(s, (cudaStream_t)stream);
+}
+
+int smk_nso_residual_norms(smk_nso* h, const smk_state* s, double* ri, double* r2, void* stream) {
+  if (!h || !s || !ri) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->norms(s, ri, r2, (cudaStream_t)stream);
+}
+
+int smk_nso_gauge_fix(smk_nso* h, const smk_state* s, void* stream) {
+  if (!h || !s) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->gauge(s, (cudaStream_t)stream);
+}
+
+int smk_nso_solve(smk_nso* h, const smk_state* s, double eps, int relative, int budget, int* cycles, double* hist,
+                  void* stream) {
+  if (!h || !s) { set_error("null argument"); return SMK_ERR_ARG; }
+  if (!(eps > 0)) { set_error("eps must be positive"); return SMK_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  double ri = 0, r2 = 0;
+  int rc = h->impl->norms(s, &ri, &r2, st);
+  if (rc) return rc;
+  if (hist) { hist[0] = ri; hist[1] = r2; }
+  double tol = relative ? eps * ri : eps;
+  if (cycles) *cycles = 0;
+  if (ri <= tol) return SMK_OK;
+  for (int c = 1; c <= budget; ++c) {
+    rc = h->impl->vcycle(s, st);
+    if (rc) return rc;
+    rc = h->impl->gauge(s, st);
+    if (rc) return rc;
+    rc = h->impl->norms(s, &ri, &r2, st);
+    if (rc) return rc;
+    if (hist) { hist[2 * c] = ri; hist[2 * c + 1] = r2; }
+    if (cycles) *cycles = c;
+    if (ri <= tol) return SMK_OK;
+  }
+  set_error("STFAS cycle budget exhausted (residual %.3e > %.3e)", ri, tol);
+  return SMK_NONCONVERGENCE;
+}
+
+int smk_kkt_residual(const smk_grid* g, const smk_nso_params* p, const smk_state* s, const void* const v0[],
+                     const void* const vstar[], const smk_residual* rhs, const smk_residual* out, void* stream) {
+  if (check_grid(g) || check_params(p)) return SMK_ERR_ARG;
+  smk_nso_params q = *p;
+  q.n_levels = 1;
+  return dispatch(g, [&](auto tag) {
+    using T = decltype(tag);
+    Nso<T::DIM, T::PER, typename T::R> n(to_geo(g), q);
+    if (!n.ok) { set_error("allocation failed"); return SMK_ERR_CUDA; }
+    n.set_guide(v0, vstar, (cudaStream_t)stream);
+    int rc = n.residual_api(s, rhs, out, (cudaStream_t)stream);
+    cudaStreamSynchronize((cudaStream_t)stream);
+    return rc;
+  });
+}
+
+int smk_scgs_sweep(const smk_grid* g, const smk_nso_params* p, const smk_state* s, const void* const v0[],
+                   const void* const vstar[], const smk_residual* rhs, void* stream) {
+  if (check_grid(g) || check_params(p)) return SMK_ERR_ARG;
+  smk_nso_params q = *p;
+  q.n_levels = 1;
+  return dispatch(g, [&](auto tag) {
+    using T = decltype(tag);
+    Nso<T::DIM, T::PER, typename T::R> n(to_geo(g), q);
+    if (!n.ok) { set_error("allocation failed"); return SMK_ERR_CUDA; }
+    n.set_guide(v0, vstar, (cudaStream_t)stream);
+    int rc = n.sweep_api(s, rhs, (cudaStream_t)stream);
+    cudaStreamSynchronize((cudaStream_t)stream);
+    return rc;
+  });
+}
+
+}  // extern "C"

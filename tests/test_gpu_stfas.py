@@ -1,0 +1,148 @@
+"""STFAS kernels on B200 vs the CPU oracle (oracle/stfas.py) on seeded inputs.
+
+fp64 bar: <= 1e-10 relative on single passes (residual, colour pass, sweep,
+V-cycle) and <= 1e-8 relative on converged fields (v, u; p and pbar modulo
+per-frame constants).  fp32 bar (stated): residual/sweep <= 1e-4 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import stfas
+from problems import make_problem, random_residual, random_state
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(2, "neumann"), (2, "periodic"), (3, "neumann"), (3, "periodic")]
+
+
+@pytest.fixture(scope="module")
+def nso():
+    from paper_1608_01102_b200 import _lib, nso
+    _lib.load()
+    return nso
+
+
+def spec_cfg(nso, pb, **kw):
+    from paper_1608_01102_b200.fields import GridSpec
+    g = pb.g
+    s = GridSpec(g.dim, g.res, g.h, g.boundary)
+    cfg = nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, omega=pb.omega, color_mod=pb.colors, **kw)
+    return s, cfg
+
+
+def to_dev(nso, st, dtype=torch.float64):
+    return nso.SpacetimeState.from_arrays(st.V, st.PB, st.U, st.P, dtype=dtype)
+
+
+def to_dev_res(nso, r, dtype=torch.float64):
+    from paper_1608_01102_b200._dev import as_dev
+    return nso.SpacetimeResidual(tuple(as_dev(c, dtype) for c in r.R1), as_dev(r.R2, dtype),
+                                 tuple(as_dev(c, dtype) for c in r.R3), as_dev(r.R4, dtype))
+
+
+def state_err(dev, st, gauge=False):
+    V, PB, U, P = dev.numpy()
+    if gauge:
+        ax = tuple(range(1, PB.ndim))
+        f = lambda x: x - x.mean(axis=ax, keepdims=True)
+        return max(rel_err(V, st.V), rel_err(U, st.U), rel_err(f(PB), f(st.PB)), rel_err(f(P), f(st.P)))
+    return max(rel_err(V, st.V), rel_err(U, st.U), rel_err(PB, st.PB), rel_err(P, st.P))
+
+
+def res_err(dev, r):
+    R1, R2, R3, R4 = dev.numpy()
+    return max(rel_err(R1, r.R1), rel_err(R2, r.R2), rel_err(R3, r.R3), rel_err(R4, r.R4))
+
+
+@pytest.mark.parametrize("dim,bnd", CASES)
+def test_kkt_residual(nso, dim, bnd):
+    pb = make_problem(dim, n=8, N=3, boundary=bnd, seed=11)
+    rng = np.random.default_rng(1)
+    st = random_state(pb, rng)
+    rhs = random_residual(pb, rng)
+    s, cfg = spec_cfg(nso, pb)
+    got = nso.kkt_residual(s, cfg, to_dev(nso, st), pb.v0, pb.vstar)
+    assert res_err(got, stfas.kkt_residual(pb, st)) < 1e-12
+    got = nso.kkt_residual(s, cfg, to_dev(nso, st), pb.v0, pb.vstar, rhs=to_dev_res(nso, rhs))
+    assert res_err(got, stfas.kkt_residual(pb, st).sub(rhs)) < 1e-12
+
+
+def test_kkt_zero_is_kkt_point_of_zero_guide(nso):
+    pb = make_problem(2, n=8, N=3, seed=2)
+    pb.vstar = tuple(np.zeros_like(c) for c in pb.vstar)
+    s, cfg = spec_cfg(nso, pb)
+    st = nso.SpacetimeState.zeros(s, 3)
+    assert nso.kkt_residual(s, cfg, st, pb.v0, pb.vstar).inf() == 0.0
+
+
+@pytest.mark.parametrize("dim,bnd", CASES)
+def test_scgs_sweep(nso, dim, bnd):
+    pb = make_problem(dim, n=8, N=3, boundary=bnd, seed=21)
+    rng = np.random.default_rng(3)
+    st = random_state(pb, rng, 0.05)
+    rhs = random_residual(pb, rng, 0.05)
+    s, cfg = spec_cfg(nso, pb)
+    want = stfas.scgs_smooth(pb, st, rhs)
+    dev = to_dev(nso, st)
+    nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar, rhs=to_dev_res(nso, rhs))
+    assert state_err(dev, want) < 1e-10
+
+
+def test_scgs_fixes_exact_solution(nso):
+    # rhs = f(x) -> smoothing leaves x unchanged
+    pb = make_problem(2, n=8, N=4, seed=5)
+    rng = np.random.default_rng(4)
+    st = random_state(pb, rng)
+    rhs = stfas.kkt_residual(pb, st)
+    s, cfg = spec_cfg(nso, pb)
+    dev = to_dev(nso, st)
+    nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar, rhs=to_dev_res(nso, rhs))
+    assert state_err(dev, st) < 1e-11
+
+
+@pytest.mark.parametrize("dim,bnd", [(2, "neumann"), (2, "periodic"), (3, "neumann")])
+def test_vcycle(nso, dim, bnd):
+    n = 16 if dim == 2 else 8
+    pb = make_problem(dim, n=n, N=4, boundary=bnd, seed=31)
+    s, cfg = spec_cfg(nso, pb)
+    levels = stfas.build_levels(pb, 2)
+    want = stfas.vcycle(levels, 0, stfas.zero_state(pb.g, pb.N))
+    cfg.n_levels = 2
+    dev = nso.SpacetimeState.zeros(s, pb.N)
+    hier = nso.StfasHierarchy(s, cfg, pb.N)
+    hier.set_guide(pb.v0, pb.vstar)
+    assert hier.levels == 2
+    hier.vcycle(dev)
+    assert state_err(dev, want) < 1e-9
+
+
+def test_solve_nso_matches_oracle_cfg1_shape(nso):
+    # 32^2 / N=16 shape of BASELINE cfg1 at small budget: same iterates
+    pb = make_problem(2, n=16, N=8, seed=41)
+    s, cfg = spec_cfg(nso, pb, n_levels=2)
+    ref = stfas.solve_nso(pb, eps=1e-9, cycle_budget=6, n_levels=2)
+    dev = nso.SpacetimeState.zeros(s, pb.N)
+    hier = nso.StfasHierarchy(s, cfg, pb.N)
+    hier.set_guide(pb.v0, pb.vstar)
+    for c in range(6):
+        hier.vcycle(dev)
+        hier.gauge_fix(dev)
+    assert state_err(dev, ref.state, gauge=True) < 1e-8
+    ri, _ = hier.residual_norms(dev)
+    assert abs(ri - ref.history[-1][1]) <= 1e-6 * ref.history[0][1]
+
+
+def test_fp32_bound(nso):
+    pb = make_problem(2, n=16, N=4, seed=51)
+    rng = np.random.default_rng(6)
+    st = random_state(pb, rng)
+    s, cfg = spec_cfg(nso, pb)
+    got = nso.kkt_residual(s, cfg, to_dev(nso, st, torch.float32), pb.v0, pb.vstar)
+    assert res_err(got, stfas.kkt_residual(pb, st)) < 1e-4
+    want = stfas.scgs_smooth(pb, st)
+    dev = to_dev(nso, st, torch.float32)
+    nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar)
+    assert state_err(dev, want) < 1e-4
