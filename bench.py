@@ -237,7 +237,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if clocks else None
-    k_ms, k_n, k_cells = hier.profile_read()
+    kprof = {name: hier.profile_read(kind) for kind, name in hier.KERNELS.items()}
     hier.profile(False)
     ms = t_total / args.steps
     if world > 1:
@@ -249,10 +249,17 @@ def main():
     value = w.cell_timesteps * world / (ms / 1000.0)
     hbm, peak_kind = peaks()
     esz = 4 if w.dtype == torch.float32 else 8
-    # dominant kernel: the smoother's colour kernel
-    k_bytes = k_cells * sweep_values(w.dim) * esz / (2 ** w.dim)   # per colour launch share of a sweep
+    # dominant kernel = the smoother kernel with the largest summed time; its
+    # algorithmic bytes are its share of the sweep traffic:
+    # (2s + g) values per cell-timestep per sweep, split evenly over the
+    # assemble / line / apply kernels of each colour pass
+    kname = max(kprof, key=lambda k: kprof[k][0])
+    k_ms, k_n, k_cells = kprof[kname]
+    k_bytes = k_cells * sweep_values(w.dim) * esz / 3.0
     k_avg_ms = k_ms / max(k_n, 1)
     k_achieved = (k_bytes / max(k_n, 1)) / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                   "share_of_step": (v[0] / args.steps) / ms if ms else None} for k, v in kprof.items()}
     vc_bytes = vcycle_values_per_cts(w.dim, hier.levels) * esz * w.cell_timesteps
     vc_gbs = vc_bytes / (ms / 1000.0) / 1e9
 
@@ -310,10 +317,11 @@ def main():
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "flushed" if flush is not None else "inputs larger than L2",
                        "residual_inf_after": ri},
-            "roofline": {"bound": "hbm", "kernel": "k_scgs_color", "achieved": k_achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": k_achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": k_achieved / hbm,
                          "traffic": None, "avg_launch_ms": k_avg_ms, "launches": k_n,
                          "share_of_step": (k_ms / args.steps) / ms if ms else None},
+            "smoother_kernels": kernels,
             "vcycle_hbm": {"achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
                            "algorithmic_bytes": vc_bytes},
             "e2e": e2e,

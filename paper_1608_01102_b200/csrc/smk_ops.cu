@@ -1275,7 +1275,8 @@ int smk_dot(int dtype, const void* x, const void* y, int64_t n, double* out, voi
 int smk_restrict_cell(const smk_grid* g, int N, const void* x, void* out, void* stream) {
   return dispatch(g, [&](auto tag) {
     using T = decltype(tag); using R = typename T::R;
-    if (!can_coarsen(to_geo(g))) { set_error("grid cannot be coarsened"); return SMK_ERR_ARG; }
+    for (int a = 0; a < g->dim; ++a)
+      if (g->res[a] % 2) { set_error("restriction needs even resolution"); return SMK_ERR_ARG; }
     launch_restrict_cell<T::DIM, T::PER, R>(to_geo(g), N, (const R*)x, (R*)out, ST(stream));
     return cuda_check("smk_restrict_cell");
   });
@@ -1292,7 +1293,8 @@ int smk_prolong_cell(const smk_grid* g, int N, const void* x, void* out, int acc
 int smk_restrict_face(const smk_grid* g, int N, const void* const in[], void* const out[], void* stream) {
   return dispatch(g, [&](auto tag) {
     using T = decltype(tag); using R = typename T::R;
-    if (!can_coarsen(to_geo(g))) { set_error("grid cannot be coarsened"); return SMK_ERR_ARG; }
+    for (int a = 0; a < g->dim; ++a)
+      if (g->res[a] % 2) { set_error("restriction needs even resolution"); return SMK_ERR_ARG; }
     launch_restrict_face<T::DIM, T::PER, R>(to_geo(g), N, face3<R>(in, g->dim), facew<R>(out, g->dim), ST(stream));
     return cuda_check("smk_restrict_face");
   });

@@ -210,46 +210,121 @@ struct Slots {
   static constexpr int C = NF + 1;  // W columns (faces) + z
 };
 
-// scratch layout: [block][entry][m] with entry = row * C + col
+// colour-cell geometry shared by the smoother kernels
 template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1,
-                                                   int o2, int mod, int m0, int m1, int m2, R omega,
-                                                   R* __restrict__ scratch, R* __restrict__ xout, int* flag) {
-  constexpr int NF = Slots<DIM>::NF, B = Slots<DIM>::B, C = Slots<DIM>::C;
-  const int64_t M = (int64_t)m0 * m1 * m2;
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
-  const auto& ix = cx.ix;
+struct CellGeo {
+  static constexpr int NF = 2 * DIM;
   int c[3];
-  {
+  int fidx[NF][3];
+  bool wall[NF];
+  R gcol[NF];
+  __device__ __forceinline__ CellGeo(const Ix<DIM, PER>& ix, R h, int64_t m, int o0, int o1, int o2, int mod, int m1,
+                                     int m2) {
     int64_t q = m;
     int q2 = (int)(q % m2); q /= m2;
     int q1 = (int)(q % m1); q /= m1;
     c[0] = o0 + mod * (int)q;
     c[1] = o1 + mod * q1;
     c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        int qq = 2 * k + s;
+        fidx[qq][0] = c[0]; fidx[qq][1] = c[1]; fidx[qq][2] = c[2];
+        fidx[qq][k] += s;
+        if (PER && fidx[qq][k] >= ix.n(k)) fidx[qq][k] -= ix.n(k);
+        wall[qq] = !PER && (s == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
+        gcol[qq] = wall[qq] ? R(0) : (s == 0 ? R(1) : R(-1)) / h;
+      }
   }
-  // local face slots q = 2k + s
-  int fidx[NF][3];
-  bool wall[NF];
-  R gcol[NF];
+};
+
+// assembled per (cell, frame) entries: yU[B], yV[B], J[NF*NF]
+template <int DIM>
+struct AsmLayout {
+  static constexpr int NF = 2 * DIM, B = NF + 1;
+  static constexpr int E = 2 * B + NF * NF;
+};
+
+// Phase 1 (parallel over colour cells x frames): local residual rows
+// -(f - rhs) of both blocks of pair i and the local Jacobian of Adv at
+// v_{i+1}.  Layout asm[(i * E + e) * M + m] (coalesced in m).
+template <int DIM, bool PER, class R>
+__global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0,
+                                                       int o1, int o2, int mod, int m0, int m1, int m2,
+                                                       R* __restrict__ asmb) {
+  constexpr int NF = AsmLayout<DIM>::NF, B = AsmLayout<DIM>::B, E = AsmLayout<DIM>::E;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const auto& ix = cx.ix;
+  SMK_GRID_STRIDE(t, (int64_t)cx.N * M) {
+    const int i = (int)(t / M);
+    const int64_t m = t - (int64_t)i * M;
+    CellGeo<DIM, PER, R> cg(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
+    R* out = asmb + (int64_t)i * E * M + m;
 #pragma unroll
-  for (int k = 0; k < DIM; ++k)
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      int q = 2 * k + s;
-      fidx[q][0] = c[0]; fidx[q][1] = c[1]; fidx[q][2] = c[2];
-      fidx[q][k] += s;
-      if (PER && fidx[q][k] >= ix.n(k)) fidx[q][k] -= ix.n(k);
-      wall[q] = !PER && (s == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
-      gcol[q] = wall[q] ? R(0) : (s == 0 ? R(1) : R(-1)) / cx.h;
+    for (int q = 0; q < NF; ++q) {
+      R yu = R(0), yv = R(0);
+      if (!cg.wall[q]) {
+        int j = q >> 1;
+        yu = cx.r3(i, j, cg.fidx[q]);
+        yv = cx.r1(i, j, cg.fidx[q]);
+        if (has_rhs) {
+          int64_t o = (int64_t)i * cx.nf[j] + ix.face_off(j, cg.fidx[q][0], cg.fidx[q][1], cg.fidx[q][2]);
+          yu -= rhs.R3[j][o];
+          yv -= rhs.R1[j][o];
+        }
+      }
+      out[(int64_t)q * M] = -yu;
+      out[(int64_t)(B + q) * M] = -yv;
     }
-  const R idt = R(1) / cx.dt;
-  const int N = cx.N;
+    {
+      R yu = cx.r4(i, cg.c), yv = cx.r2(i, cg.c);
+      if (has_rhs) {
+        int64_t o = (int64_t)i * cx.nc + ix.cell_off(cg.c[0], cg.c[1], cg.c[2]);
+        yu -= rhs.R4[o];
+        yv -= rhs.R2[o];
+      }
+      out[(int64_t)NF * M] = -yu;
+      out[(int64_t)(B + NF) * M] = -yv;
+    }
+    Face3<R> Vi = frame_of(cx.V, i, cx.nf);
+    MemField<DIM, PER, R> Av{ix, Vi};
+#pragma unroll
+    for (int qc = 0; qc < NF; ++qc) {
+      UnitField<DIM, PER, R> Eu{ix, qc >> 1, cg.fidx[qc][0], cg.fidx[qc][1], cg.fidx[qc][2]};
+#pragma unroll
+      for (int qr = 0; qr < NF; ++qr) {
+        R v = R(0);
+        if (!cg.wall[qr] && !cg.wall[qc])
+          v = S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, cg.fidx[qr], Av, Eu) +
+              S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, cg.fidx[qr], Eu, Av);
+        out[(int64_t)(2 * B + qr * NF + qc) * M] = v;
+      }
+    }
+  }
+}
+
+// Phase 2 (one thread per colour cell): block-Thomas recursion along the
+// time line over the assembled entries, back substitution, omega * dx out.
+// scratch layout: [block][entry][m] with entry = row * C + col.
+template <int DIM, bool PER, class R>
+__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, int o0, int o1, int o2,
+                                                  int mod, int m0, int m1, int m2, R omega,
+                                                  const R* __restrict__ asmb, R* __restrict__ scratch,
+                                                  R* __restrict__ xout, int* flag) {
+  constexpr int NF = Slots<DIM>::NF, B = Slots<DIM>::B, C = Slots<DIM>::C, E = AsmLayout<DIM>::E;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  CellGeo<DIM, PER, R> cg(ix, h, m, o0, o1, o2, mod, m1, m2);
+  const bool* wall = cg.wall;
+  const R* gcol = cg.gcol;
+  const R idt = R(1) / dt;
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
   bool ok = true;
-  R zprev[B];    // z of the previous block
-  R Wprev[B][NF];  // W of the previous block (face columns)
+  R zprev[B];
+  R Wprev[B][NF];
 #pragma unroll
   for (int a = 0; a < B; ++a) {
     zprev[a] = R(0);
@@ -265,24 +340,12 @@ __global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP
   };
 
   for (int i = 0; i < N; ++i) {
-    // ---- local Jacobian of Adv at v_{i+1} on the cell's faces ----
+    const R* in = asmb + (int64_t)i * E * M + m;
     R J[NF][NF];
-    {
-      Face3<R> Vi = frame_of(cx.V, i, cx.nf);
-      MemField<DIM, PER, R> Av{ix, Vi};
 #pragma unroll
-      for (int qc = 0; qc < NF; ++qc) {
-        UnitField<DIM, PER, R> E{ix, qc >> 1, fidx[qc][0], fidx[qc][1], fidx[qc][2]};
+    for (int qr = 0; qr < NF; ++qr)
 #pragma unroll
-        for (int qr = 0; qr < NF; ++qr) {
-          R v = R(0);
-          if (!wall[qr] && !wall[qc])
-            v = S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, fidx[qr], Av, E) +
-                S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, fidx[qr], E, Av);
-          J[qr][qc] = v;
-        }
-      }
-    }
+      for (int qc = 0; qc < NF; ++qc) J[qr][qc] = __ldg(in + (int64_t)(2 * B + qr * NF + qc) * M);
     // ================= u-block (rows R3[i], R4[i]; unknowns u_i, p_{i+1}) =====
     {
       R A[B][B], X[B][C];
@@ -296,22 +359,8 @@ __global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP
         A[q][NF] = gcol[q];
         A[NF][q] = -gcol[q];
       }
-      // rhs = -(f - rhs)
 #pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        R y = R(0);
-        if (!wall[q]) {
-          int j = q >> 1;
-          y = cx.r3(i, j, fidx[q]);
-          if (has_rhs) y -= rhs.R3[j][(int64_t)i * cx.nf[j] + ix.face_off(j, fidx[q][0], fidx[q][1], fidx[q][2])];
-        }
-        X[q][NF] = -y;
-      }
-      {
-        R y = cx.r4(i, c);
-        if (has_rhs) y -= rhs.R4[(int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2])];
-        X[NF][NF] = -y;
-      }
+      for (int q = 0; q < B; ++q) X[q][NF] = __ldg(in + (int64_t)q * M);
       // coupling to the previous v-block (v_i): L = -I/dt on faces
       if (i > 0) {
 #pragma unroll
@@ -339,7 +388,7 @@ __global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP
     // ================= v-block (rows R1[i], R2[i]; unknowns v_{i+1}, pbar) ====
     {
       R A[B][B], X[B][C];
-      const R alpha = (i < N - 1) ? cx.kr : R(0);
+      const R alpha = (i < N - 1) ? kr : R(0);
 #pragma unroll
       for (int r = 0; r < B; ++r)
 #pragma unroll
@@ -351,20 +400,7 @@ __global__ void __launch_bounds__(128) k_scgs_color(KktCtx<DIM, PER, R> cx, ResP
         A[NF][q] = -gcol[q];
       }
 #pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        R y = R(0);
-        if (!wall[q]) {
-          int j = q >> 1;
-          y = cx.r1(i, j, fidx[q]);
-          if (has_rhs) y -= rhs.R1[j][(int64_t)i * cx.nf[j] + ix.face_off(j, fidx[q][0], fidx[q][1], fidx[q][2])];
-        }
-        X[q][NF] = -y;
-      }
-      {
-        R y = cx.r2(i, c);
-        if (has_rhs) y -= rhs.R2[(int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2])];
-        X[NF][NF] = -y;
-      }
+      for (int q = 0; q < B; ++q) X[q][NF] = __ldg(in + (int64_t)(B + q) * M);
       // lower coupling to u_i: L = I/dt + J^T  ->  A -= L Wprev, rhs -= L zprev
 #pragma unroll
       for (int r = 0; r < NF; ++r) {
@@ -489,7 +525,7 @@ struct NsoBase {
   virtual int gauge(const smk_state* s, cudaStream_t st) = 0;
   virtual int levels() const = 0;
   virtual int profile(int enable) = 0;
-  virtual int profile_read(double* ms, long long* launches, long long* cells) = 0;
+  virtual int profile_read(int kind, double* ms, long long* launches, long long* cells) = 0;
   virtual int64_t bytes() const = 0;
 };
 
@@ -500,6 +536,7 @@ struct Nso : NsoBase {
   Scratch mem;
   int64_t nbytes = 0;
   R* scratch = nullptr;   // smoother W/z
+  R* asmb = nullptr;      // smoother assembled entries
   R* xout = nullptr;      // smoother deltas
   int* flag = nullptr;
   double* parts = nullptr;
@@ -510,9 +547,27 @@ struct Nso : NsoBase {
   bool guide_set = false;
   // optional CUDA-event profile of the smoother's colour kernel
   bool prof = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-  size_t ev_used = 0;
-  int64_t prof_cells = 0;  // cell-timesteps processed by profiled launches
+  static constexpr int NKIND = 3;  // 0 assemble, 1 line solve, 2 apply
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[NKIND];
+  size_t ev_used[NKIND] = {0, 0, 0};
+  int64_t prof_cells[NKIND] = {0, 0, 0};  // cell-timesteps processed
+
+  void prof_begin(int kind, int64_t M, cudaStream_t st) {
+    if (!prof) return;
+    if (ev_used[kind] == ev[kind].size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      ev[kind].push_back({a, b});
+    }
+    prof_cells[kind] += M * prm.n_frames;
+    cudaEventRecord(ev[kind][ev_used[kind]].first, st);
+  }
+  void prof_end(int kind, cudaStream_t st) {
+    if (!prof) return;
+    cudaEventRecord(ev[kind][ev_used[kind]].second, st);
+    ++ev_used[kind];
+  }
 
   R* alloc(int64_t n) {
     void* p = mem.get((size_t)n * sizeof(R));
@@ -560,6 +615,7 @@ struct Nso : NsoBase {
     constexpr int B = Slots<DIM>::B, C = Slots<DIM>::C;
     scratch = alloc((int64_t)2 * N * B * C * maxM);
     xout = alloc((int64_t)2 * N * B * maxM);
+    asmb = alloc((int64_t)N * AsmLayout<DIM>::E * maxM);
     flag = (int*)mem.get(64);
     parts = (double*)mem.get(sizeof(double) * 70000);
     scal = mem.get(64);
@@ -569,28 +625,32 @@ struct Nso : NsoBase {
   int levels() const override { return (int)lv.size(); }
   int profile(int enable) override {
     prof = enable != 0;
-    ev_used = 0;
-    prof_cells = 0;
+    for (int k = 0; k < NKIND; ++k) {
+      ev_used[k] = 0;
+      prof_cells[k] = 0;
+    }
     return SMK_OK;
   }
-  int profile_read(double* ms, long long* launches, long long* cells) override {
+  int profile_read(int kind, double* ms, long long* launches, long long* cells) override {
+    if (kind < 0 || kind >= NKIND) { set_error("bad profile kind"); return SMK_ERR_ARG; }
     double tot = 0.0;
-    for (size_t i = 0; i < ev_used; ++i) {
-      cudaEventSynchronize(ev[i].second);
+    for (size_t i = 0; i < ev_used[kind]; ++i) {
+      cudaEventSynchronize(ev[kind][i].second);
       float t = 0.f;
-      cudaEventElapsedTime(&t, ev[i].first, ev[i].second);
+      cudaEventElapsedTime(&t, ev[kind][i].first, ev[kind][i].second);
       tot += t;
     }
     if (ms) *ms = tot;
-    if (launches) *launches = (long long)ev_used;
-    if (cells) *cells = (long long)prof_cells;
+    if (launches) *launches = (long long)ev_used[kind];
+    if (cells) *cells = (long long)prof_cells[kind];
     return cuda_check("nso_profile_read");
   }
   ~Nso() override {
-    for (auto& e : ev) {
-      cudaEventDestroy(e.first);
-      cudaEventDestroy(e.second);
-    }
+    for (int k = 0; k < NKIND; ++k)
+      for (auto& e : ev[k]) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
   }
   int64_t bytes() const override { return nbytes; }
 
@@ -655,26 +715,22 @@ struct Nso : NsoBase {
       }
       int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
       if (M == 0) continue;
-      cudaEvent_t e1 = nullptr, e2 = nullptr;
-      if (prof) {
-        if (ev_used == ev.size()) {
-          cudaEvent_t a, b;
-          cudaEventCreate(&a);
-          cudaEventCreate(&b);
-          ev.push_back({a, b});
-        }
-        e1 = ev[ev_used].first;
-        e2 = ev[ev_used].second;
-        ++ev_used;
-        prof_cells += M * prm.n_frames;
-        cudaEventRecord(e1, st);
-      }
-      k_scgs_color<DIM, PER, R><<<(unsigned)((M + 127) / 128), 128, 0, st>>>(
-          c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout, flag); count_launch();
-      if (prof) cudaEventRecord(e2, st);
       int64_t tot = (int64_t)prm.n_frames * M;
+      prof_begin(0, M, st);
+      k_scgs_assemble<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod,
+                                                                       mm[0], mm[1], mm[2], asmb); count_launch();
+      prof_end(0, st);
+      // latency-bound recursion: spread small colours over all SMs
+      int tpb = M >= 148 * 128 ? 128 : 32;
+      prof_begin(1, M, st);
+      k_scgs_line<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(
+          ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+          (R)prm.omega, asmb, scratch, xout, flag); count_launch();
+      prof_end(1, st);
+      prof_begin(2, M, st);
       k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
                                                                      mm[1], mm[2], xout); count_launch();
+      prof_end(2, st);
     }
   }
 
@@ -927,9 +983,9 @@ int smk_nso_profile(smk_nso* h, int enable) {
   return h->impl->profile(enable);
 }
 
-int smk_nso_profile_read(smk_nso* h, double* ms, long long* launches, long long* cells) {
+int smk_nso_profile_read(smk_nso* h, int kind, double* ms, long long* launches, long long* cells) {
   if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
-  return h->impl->profile_read(ms, launches, cells);
+  return h->impl->profile_read(kind, ms, launches, cells);
 }
 int64_t smk_nso_device_bytes(const smk_nso* h) { return h ? h->impl->bytes() : 0; }
 

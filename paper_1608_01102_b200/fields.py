@@ -135,6 +135,24 @@ def _prep(spec, *args):
     return numpy, dt, conv
 
 
+class _Coarse:
+    """Shape-only view of the half-resolution grid (no >= 4 validation, like
+    the reference's restrict_cell which only needs even extents)."""
+
+    def __init__(self, spec):
+        if any(r % 2 for r in spec.res):
+            raise ValueError("restriction needs even resolution")
+        self.dim = spec.dim
+        self.res = tuple(r // 2 for r in spec.res)
+        self.periodic = spec.periodic
+
+    def face_shape(self, axis):
+        s = list(self.res)
+        if not self.periodic:
+            s[axis] += 1
+        return tuple(s)
+
+
 def _face_like(spec, lead, dt):
     return tuple(torch.empty(lead + spec.face_shape(k), dtype=dt, device="cuda") for k in range(spec.dim))
 
@@ -215,9 +233,7 @@ def dot_fields(a, b):
 def restrict_cell(spec_fine, x):
     numpy, dt, (xx,) = _prep(spec_fine, x)
     n, lead = _frames(spec_fine, xx)
-    gc = spec_fine.coarsen()
-    if gc is None:
-        raise ValueError("grid cannot be coarsened")
+    gc = _Coarse(spec_fine)
     out = torch.empty(lead + gc.res, dtype=dt, device="cuda")
     L = _lib.load()
     _lib.check(L.smk_restrict_cell(_dev.grid(spec_fine, dt), n, xx.data_ptr(), out.data_ptr(), _dev.stream()))
@@ -238,9 +254,7 @@ def restrict_face(spec_fine, comps):
     """STFAS face restriction."""
     numpy, dt, (c,) = _prep(spec_fine, comps)
     n, lead = _frames(spec_fine, c[0])
-    gc = spec_fine.coarsen()
-    if gc is None:
-        raise ValueError("grid cannot be coarsened")
+    gc = _Coarse(spec_fine)
     out = _face_like(gc, lead, dt)
     L = _lib.load()
     _lib.check(L.smk_restrict_face(_dev.grid(spec_fine, dt), n, _lib.ptrs(c), _lib.ptrs(out), _dev.stream()))

@@ -242,11 +242,13 @@ class StfasHierarchy:
     def profile(self, enable=True):
         _lib.check(self._L.smk_nso_profile(self._h, int(bool(enable))), "profile")
 
-    def profile_read(self):
-        """(smoother colour-kernel ms summed, launches, cell-timesteps)."""
+    KERNELS = {0: "k_scgs_assemble", 1: "k_scgs_line", 2: "k_scgs_apply"}
+
+    def profile_read(self, kind=1):
+        """(summed kernel ms, launches, cell-timesteps) for smoother kernel `kind`."""
         ms, n, cells = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
-        _lib.check(self._L.smk_nso_profile_read(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(cells)),
-                   "profile_read")
+        _lib.check(self._L.smk_nso_profile_read(self._h, int(kind), ctypes.byref(ms), ctypes.byref(n),
+                                                ctypes.byref(cells)), "profile_read")
         return ms.value, n.value, cells.value
 
     def set_guide(self, v0, vstar):
