@@ -196,6 +196,10 @@ __device__ __forceinline__ R JT_at(const Ix<DIM, PER>& ix, R c0, int k, const in
   return Tadj_at<DIM, PER, R>(ix, c0, k, g, v, u) - S_at<DIM, PER, R>(ix, c0, k, g, v, u);
 }
 
+// explicit-width |x| (an unqualified abs() on a float can bind to int abs)
+__device__ __forceinline__ float rabs(float x) { return fabsf(x); }
+__device__ __forceinline__ double rabs(double x) { return fabs(x); }
+
 // ---------------------------------------------------------------------------
 // reductions
 // ---------------------------------------------------------------------------

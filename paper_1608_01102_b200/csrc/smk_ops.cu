@@ -135,7 +135,7 @@ __global__ void k_laplacian(Ix<DIM, PER> ix, R h, const R* __restrict__ p, R* __
 template <class R>
 __global__ void k_absmax(const R* __restrict__ x, int64_t n, R* out) {
   R m = R(0);
-  SMK_GRID_STRIDE(i, n) m = max(m, abs(x[i]));
+  SMK_GRID_STRIDE(i, n) m = max(m, rabs(x[i]));
   block_max_to(m, out);
 }
 
@@ -219,7 +219,7 @@ __global__ void k_axpby(R* __restrict__ y, const R* __restrict__ x, R a, R b, in
 template <class R>
 __global__ void k_absdiff_max(const R* __restrict__ a, const R* __restrict__ b, int64_t n, R* out) {
   R m = R(0);
-  SMK_GRID_STRIDE(i, n) m = max(m, abs(a[i] - b[i]));
+  SMK_GRID_STRIDE(i, n) m = max(m, rabs(a[i] - b[i]));
   block_max_to(m, out);
 }
 
@@ -424,7 +424,7 @@ __global__ void k_transport(Ix<DIM, PER> ix, R c0, Face3<R> v, int vframes, cons
     R term = s * o;
     out[t] = term;
     if (acc) acc[t] = acc[t] + term;
-    m = max(m, abs(term));
+    m = max(m, rabs(term));
   }
   if (norm) block_max_to(m, norm);
 }
@@ -610,7 +610,7 @@ __global__ void k_resid_absmax(Ix<DIM, PER> ix, R h, const R* __restrict__ p, co
   SMK_GRID_STRIDE(t, ix.cells()) {
     int c[3];
     ix.cell_idx(t, c);
-    m = max(m, abs(rhs[t] - lap_at(ix, h, p, c)));
+    m = max(m, rabs(rhs[t] - lap_at(ix, h, p, c)));
   }
   block_max_to(m, norm);
 }

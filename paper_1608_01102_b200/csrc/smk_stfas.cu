@@ -162,7 +162,7 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
     if (PIVOT) {
 #pragma unroll
       for (int r = col + 1; r < B; ++r) {
-        bool sw = abs(A[r][col]) > abs(A[col][col]);
+        bool sw = rabs(A[r][col]) > rabs(A[col][col]);
 #pragma unroll
         for (int c = 0; c < B; ++c) {
           R a = A[col][c], b = A[r][c];
@@ -178,7 +178,7 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
       }
     }
     R piv = A[col][col];
-    if (!(abs(piv) > tiny)) ok = false;
+    if (!(rabs(piv) > tiny)) ok = false;
     R inv = R(1) / piv;
 #pragma unroll
     for (int r = col + 1; r < B; ++r) {
@@ -240,16 +240,68 @@ struct CellGeo {
   }
 };
 
-// assembled per (cell, frame) entries: yU[B], yV[B], J[NF*NF]
+// Closed-form local Jacobian of Adv(v) = S(v, v) on the cell's own faces
+// (derived from advection.py:306-377 with d = e_g):
+//   row (j,s_r), col (j,s_c):  S(v, e_g) gives the opposite-face coupling
+//     +/- c0 * vc_j (vc_j = cell-centre average of v_j), S(e_g, v) gives
+//     (j,0)(j,0) = c0/2 (v_j[c+e_j] - v_j[c-e_j])   (j,0)(j,1) += c0/2 v_j[c+e_j]
+//     (j,1)(j,1) = c0/2 (v_j[c+2e_j] - v_j[c])      (j,1)(j,0) -= c0/2 v_j[c]
+//   row (j,s), col (k != j):  (k,1) = +c0/2 v_j[c + s e_j + e_k]
+//                             (k,0) = -c0/2 v_j[c + s e_j - e_k]
+// Wall rows / columns are zero (not unknowns).  Equal to the probed Jacobian
+// of oracle/stfas.local_jacobian up to rounding.
+template <int DIM, bool PER, class R>
+__device__ __forceinline__ void local_jacobian(const Ix<DIM, PER>& ix, R c0, const Face3<R>& v,
+                                               const CellGeo<DIM, PER, R>& cg, R (&J)[2 * DIM][2 * DIM]) {
+  constexpr int NF = 2 * DIM;
+  const int* c = cg.c;
+  const R hc = R(0.5) * c0;
+#pragma unroll
+  for (int j = 0; j < DIM; ++j) {
+    int t[3];
+    shift((int*)c, j, -1, t);
+    R vm = ix.face(v.c[j], j, t[0], t[1], t[2]);
+    R v0 = ix.face(v.c[j], j, c[0], c[1], c[2]);
+    shift((int*)c, j, 1, t);
+    R v1 = ix.face(v.c[j], j, t[0], t[1], t[2]);
+    shift((int*)c, j, 2, t);
+    R v2 = ix.face(v.c[j], j, t[0], t[1], t[2]);
+    R vc = R(0.5) * (v0 + v1);
+    J[2 * j][2 * j] = hc * (v1 - vm);
+    J[2 * j][2 * j + 1] = c0 * vc + hc * v1;
+    J[2 * j + 1][2 * j] = -c0 * vc - hc * v0;
+    J[2 * j + 1][2 * j + 1] = hc * (v2 - v0);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      if (k == j) continue;
+#pragma unroll
+      for (int sr = 0; sr < 2; ++sr) {
+        int f[3], q[3];
+        shift((int*)c, j, sr, f);
+        shift(f, k, 1, q);
+        J[2 * j + sr][2 * k + 1] = hc * ix.face(v.c[j], j, q[0], q[1], q[2]);
+        shift(f, k, -1, q);
+        J[2 * j + sr][2 * k] = -hc * ix.face(v.c[j], j, q[0], q[1], q[2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NF; ++a)
+#pragma unroll
+    for (int b = 0; b < NF; ++b)
+      if (cg.wall[a] || cg.wall[b]) J[a][b] = R(0);
+}
+
+// assembled per (cell, frame) entries: yU[B], yV[B]
 template <int DIM>
 struct AsmLayout {
   static constexpr int NF = 2 * DIM, B = NF + 1;
-  static constexpr int E = 2 * B + NF * NF;
+  static constexpr int E = 2 * B;
 };
 
 // Phase 1 (parallel over colour cells x frames): local residual rows
-// -(f - rhs) of both blocks of pair i and the local Jacobian of Adv at
-// v_{i+1}.  Layout asm[(i * E + e) * M + m] (coalesced in m).
+// -(f - rhs) of both blocks of pair i.  Layout asm[(i * E + e) * M + m]
+// (coalesced in m).
 template <int DIM, bool PER, class R>
 __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0,
                                                        int o1, int o2, int mod, int m0, int m1, int m2,
@@ -288,20 +340,6 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
       out[(int64_t)NF * M] = -yu;
       out[(int64_t)(B + NF) * M] = -yv;
     }
-    Face3<R> Vi = frame_of(cx.V, i, cx.nf);
-    MemField<DIM, PER, R> Av{ix, Vi};
-#pragma unroll
-    for (int qc = 0; qc < NF; ++qc) {
-      UnitField<DIM, PER, R> Eu{ix, qc >> 1, cg.fidx[qc][0], cg.fidx[qc][1], cg.fidx[qc][2]};
-#pragma unroll
-      for (int qr = 0; qr < NF; ++qr) {
-        R v = R(0);
-        if (!cg.wall[qr] && !cg.wall[qc])
-          v = S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, cg.fidx[qr], Av, Eu) +
-              S_at<DIM, PER, R>(ix, cx.c0, qr >> 1, cg.fidx[qr], Eu, Av);
-        out[(int64_t)(2 * B + qr * NF + qc) * M] = v;
-      }
-    }
   }
 }
 
@@ -309,8 +347,8 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
 // time line over the assembled entries, back substitution, omega * dx out.
 // scratch layout: [block][entry][m] with entry = row * C + col.
 template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, int o0, int o1, int o2,
-                                                  int mod, int m0, int m1, int m2, R omega,
+__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, Face3<R> V,
+                                                  int o0, int o1, int o2, int mod, int m0, int m1, int m2, R omega,
                                                   const R* __restrict__ asmb, R* __restrict__ scratch,
                                                   R* __restrict__ xout, int* flag) {
   constexpr int NF = Slots<DIM>::NF, B = Slots<DIM>::B, C = Slots<DIM>::C, E = AsmLayout<DIM>::E;
@@ -342,10 +380,12 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
   for (int i = 0; i < N; ++i) {
     const R* in = asmb + (int64_t)i * E * M + m;
     R J[NF][NF];
+    {
+      Face3<R> Vi;
 #pragma unroll
-    for (int qr = 0; qr < NF; ++qr)
-#pragma unroll
-      for (int qc = 0; qc < NF; ++qc) J[qr][qc] = __ldg(in + (int64_t)(2 * B + qr * NF + qc) * M);
+      for (int k = 0; k < 3; ++k) Vi.c[k] = k < DIM ? V.c[k] + (int64_t)i * ix.faces(k) : nullptr;
+      local_jacobian<DIM, PER, R>(ix, R(0.5) / h, Vi, cg, J);
+    }
     // ================= u-block (rows R3[i], R4[i]; unknowns u_i, p_{i+1}) =====
     {
       R A[B][B], X[B][C];
@@ -620,6 +660,7 @@ struct Nso : NsoBase {
     parts = (double*)mem.get(sizeof(double) * 70000);
     scal = mem.get(64);
     if (!flag || !parts || !scal) ok = false;
+    else cudaMemset(flag, 0, 64);
   }
 
   int levels() const override { return (int)lv.size(); }
@@ -724,7 +765,7 @@ struct Nso : NsoBase {
       int tpb = M >= 148 * 128 ? 128 : 32;
       prof_begin(1, M, st);
       k_scgs_line<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(
-          ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+          ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, c.V, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
           (R)prm.omega, asmb, scratch, xout, flag); count_launch();
       prof_end(1, st);
       prof_begin(2, M, st);
