@@ -136,13 +136,18 @@ def test_solve_nso_matches_oracle_cfg1_shape(nso):
 
 
 def test_fp32_bound(nso):
+    """fp32 mode bound (stated): residual rows <= 1e-6 relative on a random
+    state; one sweep from a mid-solve state (after one fp64 V-cycle) <= 1e-4
+    relative.  (A sweep from a random state is not used: the last frame's
+    local systems carry no K anchor and amplify random residuals ~1e6x.)"""
     pb = make_problem(2, n=16, N=4, seed=51)
     rng = np.random.default_rng(6)
     st = random_state(pb, rng)
     s, cfg = spec_cfg(nso, pb)
     got = nso.kkt_residual(s, cfg, to_dev(nso, st, torch.float32), pb.v0, pb.vstar)
-    assert res_err(got, stfas.kkt_residual(pb, st)) < 1e-4
-    want = stfas.scgs_smooth(pb, st)
-    dev = to_dev(nso, st, torch.float32)
+    assert res_err(got, stfas.kkt_residual(pb, st)) < 1e-6
+    mid = stfas.vcycle(stfas.build_levels(pb, 2), 0, stfas.zero_state(pb.g, pb.N))
+    want = stfas.scgs_smooth(pb, mid)
+    dev = to_dev(nso, mid, torch.float32)
     nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar)
     assert state_err(dev, want) < 1e-4
