@@ -220,6 +220,7 @@ def main():
     clocks = Clocks(local) if rank == 0 else None
     hier.profile(True)
     n0 = L.smk_launch_count()
+    torch.cuda.profiler.start()   # ncu --profile-from-start off sees only this region
     t_total = 0.0
     for _ in range(args.steps):
         if flush is not None:
@@ -233,6 +234,7 @@ def main():
         e1.synchronize()
         t_total += e0.elapsed_time(e1)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     launches = L.smk_launch_count() - n0
     if world > 1:
         dist.barrier()
