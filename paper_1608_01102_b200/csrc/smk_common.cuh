@@ -11,6 +11,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+#include <utility>
+
 namespace smk {
 
 struct Geo {
@@ -107,6 +110,138 @@ struct UnitField {  // e_{(k*, c*)}: 1 at one face (indices already canonical)
 
 __device__ __forceinline__ void shift(int c[3], int a, int s, int out[3]) {
   out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[a] += s;
+}
+
+// ---------------------------------------------------------------------------
+// Register cache of one face field around a cell c.  Every read that S(a,w)
+// and J_Adv(v)^T u make at the cell's own 2d faces falls in 4 + 4(d-1)
+// offsets per component a:  t e_a (t = -1..2)  and  s e_a +/- e_b
+// (s = 0,1; b != a).  Slots are resolved at compile time after inlining
+// (offsets relative to c are constants), so the cache lives in registers.
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct NbrSlots {
+  static constexpr int NB = 4 + 4 * (DIM - 1);
+  // slot of offset d (relative to c) for component a, or -1 (branch-light so
+  // it folds to a constant when the offsets are compile-time)
+  __host__ __device__ __forceinline__ static int slot(int a, int d0, int d1, int d2) {
+    const int da = a == 0 ? d0 : (a == 1 ? d1 : d2);
+    // the two other axes in increasing order
+    const int b0 = a == 0 ? 1 : 0;
+    const int b1 = a == 2 ? 1 : 2;
+    const int e0 = b0 == 0 ? d0 : (b0 == 1 ? d1 : d2);
+    const int e1 = DIM == 3 ? (b1 == 1 ? d1 : d2) : 0;
+    if (DIM == 2 && d2 != 0) return -1;
+    if (e0 == 0 && e1 == 0) return (da >= -1 && da <= 2) ? da + 1 : -1;
+    if (da != 0 && da != 1) return -1;
+    if (e1 == 0 && (e0 == 1 || e0 == -1)) return 4 + 2 * da + (e0 > 0 ? 1 : 0);
+    if (DIM == 3 && e0 == 0 && (e1 == 1 || e1 == -1)) return 8 + 2 * da + (e1 > 0 ? 1 : 0);
+    return -1;
+  }
+  __host__ __device__ __forceinline__ static void offset(int a, int sl, int d[3]) {
+    d[0] = d[1] = d[2] = 0;
+    if (sl < 4) { d[a] = sl - 1; return; }
+    int r = sl - 4, bi = r / 4, rem = r % 4;
+    int b = bi < a ? bi : bi + 1;
+    d[a] = rem / 2;
+    d[b] = (rem & 1) ? 1 : -1;
+  }
+};
+
+// compile-time loop helper
+template <class F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// slot of (own-axis offset da of component a, offset db along axis b != a)
+template <int DIM>
+__host__ __device__ constexpr int nbr_slot(int a, int da, int b, int db) {
+  return db == 0 ? da + 1 : 4 + 4 * (b < a ? b : b - 1) + 2 * da + (db > 0 ? 1 : 0);
+}
+
+template <int DIM, bool PER, class R>
+struct NbrField {
+  static constexpr int NB = NbrSlots<DIM>::NB;
+  const Ix<DIM, PER>& ix;
+  int c0, c1, c2;
+  Face3<R> f;
+  R val[DIM][NB];
+  __device__ __forceinline__ NbrField(const Ix<DIM, PER>& ix_, const int c[3], const Face3<R>& f_)
+      : ix(ix_), c0(c[0]), c1(c[1]), c2(c[2]), f(f_) {
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int sl = 0; sl < NB; ++sl) {
+        int d[3];
+        NbrSlots<DIM>::offset(a, sl, d);
+        val[a][sl] = ix.face(f.c[a], a, c0 + d[0], c1 + d[1], c2 + d[2]);
+      }
+  }
+  __device__ __forceinline__ R operator()(int k, int i, int j, int l) const {
+    int sl = NbrSlots<DIM>::slot(k, i - c0, j - c1, DIM == 3 ? l - c2 : 0);
+    if (sl < 0) return ix.face(f.c[k], k, i, j, l);   // never taken on the cell's own faces
+    return val[k][sl];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Closed-form S(v,w)_J, T(v,u)_J at the cell's own J-face f = c + SD e_J from
+// register caches (same arithmetic as S_at / Tadj_at, compile-time slots).
+// Valid for non-wall faces (Neumann: both cells of the face exist).
+// ---------------------------------------------------------------------------
+template <int DIM, int J, int SD, class R>
+__device__ __forceinline__ R S_cached(R c0, const R (&A)[DIM][NbrSlots<DIM>::NB],
+                                      const R (&W)[DIM][NbrSlots<DIM>::NB], bool has_up, bool has_dn) {
+  R acc = R(0);
+  static_for<DIM>([&](auto kc) {
+    constexpr int K = decltype(kc)::value;
+    R ap, am, wp, wm;
+    if constexpr (K == J) {
+      const R aj = A[J][SD + 1];
+      ap = has_up ? R(0.5) * (aj + A[J][SD + 2]) : R(0);
+      am = has_dn ? R(0.5) * (A[J][SD] + aj) : R(0);
+      wp = W[J][SD + 2];
+      wm = W[J][SD];
+    } else {
+      ap = R(0.5) * (A[K][nbr_slot<DIM>(K, 1, J, SD)] + A[K][nbr_slot<DIM>(K, 1, J, SD - 1)]);
+      am = R(0.5) * (A[K][nbr_slot<DIM>(K, 0, J, SD)] + A[K][nbr_slot<DIM>(K, 0, J, SD - 1)]);
+      wp = W[J][nbr_slot<DIM>(J, SD, K, 1)];
+      wm = W[J][nbr_slot<DIM>(J, SD, K, -1)];
+    }
+    acc += ap * wp - am * wm;
+  });
+  return c0 * acc;
+}
+
+template <int DIM, int J, int SD, class R>
+__device__ __forceinline__ R T_cached(R c0, const R (&V)[DIM][NbrSlots<DIM>::NB],
+                                      const R (&U)[DIM][NbrSlots<DIM>::NB]) {
+  R acc = R(0);
+  static_for<DIM>([&](auto jc) {
+    constexpr int Q = decltype(jc)::value;
+    R s = R(0);
+    if constexpr (Q == J) {
+      // cells g and g - e_J: gam = c0 (u[c'] v[c'+e] - u[c'+e] v[c'])
+      static_for<2>([&](auto sc) {
+        constexpr int SIDE = decltype(sc)::value;
+        constexpr int lo = SD - SIDE + 1, hi = SD - SIDE + 2;
+        s += U[J][lo] * V[J][hi] - U[J][hi] * V[J][lo];
+      });
+    } else {
+      static_for<2>([&](auto sc) {
+        constexpr int SIDE = decltype(sc)::value;
+        constexpr int f = nbr_slot<DIM>(Q, SIDE, J, SD), fm = nbr_slot<DIM>(Q, SIDE, J, SD - 1);
+        s += U[Q][fm] * V[Q][f] - U[Q][f] * V[Q][fm];
+      });
+    }
+    acc += R(0.5) * c0 * s;
+  });
+  return acc;
 }
 
 // ---------------------------------------------------------------------------

@@ -314,26 +314,58 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
     const int64_t m = t - (int64_t)i * M;
     CellGeo<DIM, PER, R> cg(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
     R* out = asmb + (int64_t)i * E * M + m;
-#pragma unroll
-    for (int q = 0; q < NF; ++q) {
+    const int* c = cg.c;
+    Face3<R> Vi = frame_of(cx.V, i, cx.nf);
+    Face3<R> Ui = frame_of(cx.U, i, cx.nf);
+    Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
+    const bool inner = i < cx.N - 1;
+    Face3<R> Un = inner ? frame_of(cx.U, i + 1, cx.nf) : Vi;
+    Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Vi;
+    NbrField<DIM, PER, R> VC(ix, c, Vi), UC(ix, c, Ui);
+    const R* Pi = cx.P + (int64_t)i * cx.nc;
+    const R* PBi = cx.PB + (int64_t)i * cx.nc;
+    const R pc = ix.cell(Pi, c[0], c[1], c[2]), pbc = ix.cell(PBi, c[0], c[1], c[2]);
+    static_for<NF>([&](auto qc) {
+      constexpr int q = decltype(qc)::value;
+      constexpr int j = q >> 1, sd = q & 1;
       R yu = R(0), yv = R(0);
       if (!cg.wall[q]) {
-        int j = q >> 1;
-        yu = cx.r3(i, j, cg.fidx[q]);
-        yv = cx.r1(i, j, cg.fidx[q]);
+        int nb[3] = {c[0], c[1], c[2]};
+        nb[j] += sd ? 1 : -1;                         // the other cell of the face
+        const R pn = ix.cell(Pi, nb[0], nb[1], nb[2]), pbn = ix.cell(PBi, nb[0], nb[1], nb[2]);
+        const R gp = sd ? (pn - pc) / cx.h : (pc - pn) / cx.h;
+        const R gpb = sd ? (pbn - pbc) / cx.h : (pbc - pbn) / cx.h;
+        const R vf = VC.val[j][sd + 1], uf = UC.val[j][sd + 1];
+        const int64_t o = ix.face_off(j, cg.fidx[q][0], cg.fidx[q][1], cg.fidx[q][2]);
+        // cells above / below the face exist for every non-wall face
+        const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC.val, VC.val, true, true);
+        yu = (((vf - Vp.c[j][o]) / cx.dt + adv) - uf) + gp;
+        R t1 = R(0);
+        if (inner) t1 = cx.kr * (vf - Vs.c[j][o]) - Un.c[j][o] / cx.dt;
+        const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC.val, UC.val) -
+                     S_cached<DIM, j, sd, R>(cx.c0, VC.val, UC.val, true, true);
+        yv = ((t1 + uf / cx.dt) + jt) + gpb;
         if (has_rhs) {
-          int64_t o = (int64_t)i * cx.nf[j] + ix.face_off(j, cg.fidx[q][0], cg.fidx[q][1], cg.fidx[q][2]);
-          yu -= rhs.R3[j][o];
-          yv -= rhs.R1[j][o];
+          const int64_t oo = (int64_t)i * cx.nf[j] + o;
+          yu -= rhs.R3[j][oo];
+          yv -= rhs.R1[j][oo];
         }
       }
       out[(int64_t)q * M] = -yu;
       out[(int64_t)(B + q) * M] = -yv;
-    }
+    });
     {
-      R yu = cx.r4(i, cg.c), yv = cx.r2(i, cg.c);
+      R dv = R(0), du = R(0);
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        R a = (VC.val[k][2] - VC.val[k][1]) / cx.h;
+        R b = (UC.val[k][2] - UC.val[k][1]) / cx.h;
+        dv = (k == 0) ? a : dv + a;
+        du = (k == 0) ? b : du + b;
+      }
+      R yu = du, yv = dv;
       if (has_rhs) {
-        int64_t o = (int64_t)i * cx.nc + ix.cell_off(cg.c[0], cg.c[1], cg.c[2]);
+        int64_t o = (int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2]);
         yu -= rhs.R4[o];
         yv -= rhs.R2[o];
       }
@@ -343,9 +375,45 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
   }
 }
 
-// Phase 2 (one thread per colour cell): block-Thomas recursion along the
-// time line over the assembled entries, back substitution, omega * dx out.
-// scratch layout: [block][entry][m] with entry = row * C + col.
+// Phase 2 (one thread per colour cell): the cell's 2N-block Eq. 9 time line,
+// solved exactly with the u-blocks eliminated in closed form.
+//
+// The u-block of pair i is the constant saddle [[-I, g], [-g^T, 0]] (g = the
+// cell's grad column), coupled to v_i by -I/dt and to v_{i+1} by
+// M_i = I/dt + J_i.  With P = I - g g^T / sigma (sigma = g^T g):
+//     du_i = -c_i - (P/dt) dv_i + P M_i dv_{i+1},   c_i = P yu_i + g yp_i / sigma,
+//     dp_{i+1} = (g^T a_i - yp_i) / sigma,   a_i = yu_i + dv_i/dt - M_i dv_{i+1}.
+// Substituting into the v-rows leaves a symmetric block-tridiagonal system in
+// (dv_{i+1}, dpbar_{i+1}) only (N blocks instead of 2N):
+//     D_i  = M_i^T P M_i + alpha_i I + [i+1<N] P/dt^2     (faces; + the g saddle)
+//     L_i  = -M_i^T P / dt     (to dv_i),   U_i = L_{i+1}^T = -P M_{i+1} / dt
+//     rhs  = yv_i + M_i^T c_i - [i+1<N] c_{i+1} / dt.
+// This is exact block elimination of the oracle's system (oracle/stfas.py
+// block_thomas), so iterates agree to rounding.  Fill-in per pair: W (B x NF)
+// and z (B), layout [pair][entry][m].
+template <int DIM, bool PER, class R>
+__device__ __forceinline__ void load_rows(const R* __restrict__ in, int64_t M, R (&yu)[2 * DIM + 1],
+                                          R (&yv)[2 * DIM + 1]) {
+  constexpr int B = 2 * DIM + 1;
+#pragma unroll
+  for (int q = 0; q < B; ++q) {
+    yu[q] = __ldg(in + (int64_t)q * M);
+    yv[q] = __ldg(in + (int64_t)(B + q) * M);
+  }
+}
+
+template <int DIM, bool PER, class R>
+__device__ __forceinline__ void frame_M(const Ix<DIM, PER>& ix, R c0, const Face3<R>& V, int i,
+                                        const CellGeo<DIM, PER, R>& cg, R idt, R (&Mx)[2 * DIM][2 * DIM]) {
+  Face3<R> Vi;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) Vi.c[k] = k < DIM ? V.c[k] + (int64_t)i * ix.faces(k) : nullptr;
+  local_jacobian<DIM, PER, R>(ix, c0, Vi, cg, Mx);
+#pragma unroll
+  for (int q = 0; q < 2 * DIM; ++q)
+    if (!cg.wall[q]) Mx[q][q] += idt;
+}
+
 template <int DIM, bool PER, class R>
 __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, Face3<R> V,
                                                   int o0, int o1, int o2, int mod, int m0, int m1, int m2, R omega,
@@ -356,10 +424,22 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   CellGeo<DIM, PER, R> cg(ix, h, m, o0, o1, o2, mod, m1, m2);
-  const bool* wall = cg.wall;
-  const R* gcol = cg.gcol;
+  const R c0 = R(0.5) / h;
   const R idt = R(1) / dt;
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+  R sigma = R(0);
+#pragma unroll
+  for (int q = 0; q < NF; ++q) sigma += cg.gcol[q] * cg.gcol[q];
+  const R isig = R(1) / sigma;
+  // P x = x - g (g^T x) / sigma on non-wall slots (g is zero on walls)
+  auto projP = [&](R (&x)[NF]) {
+    R d = R(0);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) d += cg.gcol[q] * x[q];
+    d *= isig;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) x[q] = cg.wall[q] ? R(0) : x[q] - cg.gcol[q] * d;
+  };
   bool ok = true;
   R zprev[B];
   R Wprev[B][NF];
@@ -369,123 +449,165 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
 #pragma unroll
     for (int b = 0; b < NF; ++b) Wprev[a][b] = R(0);
   }
-  auto store = [&](int blk, R (&X)[B][C]) {
-    R* base = scratch + (int64_t)blk * B * C * M + m;
+  R Mc[NF][NF];   // M_i for the current pair
+  frame_M<DIM, PER, R>(ix, c0, V, 0, cg, idt, Mc);
+  R cc[NF];       // c_i
+  {
+    R yu[B], yv[B];
+    load_rows<DIM, PER, R>(asmb + m, M, yu, yv);
 #pragma unroll
-    for (int r = 0; r < B; ++r)
+    for (int q = 0; q < NF; ++q) cc[q] = yu[q];
+    projP(cc);
 #pragma unroll
-      for (int q = 0; q < C; ++q) base[(int64_t)(r * C + q) * M] = X[r][q];
-  };
+    for (int q = 0; q < NF; ++q) cc[q] += cg.gcol[q] * yu[NF] * isig;
+  }
 
   for (int i = 0; i < N; ++i) {
-    const R* in = asmb + (int64_t)i * E * M + m;
-    R J[NF][NF];
-    {
-      Face3<R> Vi;
+    const bool has_next = i + 1 < N;
+    R yu[B], yv[B];
+    load_rows<DIM, PER, R>(asmb + (int64_t)i * E * M + m, M, yu, yv);
+    // PM = P M_i (column-wise projection)
+    R PM[NF][NF];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) Vi.c[k] = k < DIM ? V.c[k] + (int64_t)i * ix.faces(k) : nullptr;
-      local_jacobian<DIM, PER, R>(ix, R(0.5) / h, Vi, cg, J);
+    for (int b = 0; b < NF; ++b) {
+      R col[NF];
+#pragma unroll
+      for (int a = 0; a < NF; ++a) col[a] = Mc[a][b];
+      projP(col);
+#pragma unroll
+      for (int a = 0; a < NF; ++a) PM[a][b] = col[a];
     }
-    // ================= u-block (rows R3[i], R4[i]; unknowns u_i, p_{i+1}) =====
-    {
-      R A[B][B], X[B][C];
+    R A[B][B], X[B][C];
+    const R alpha = (i < N - 1) ? kr : R(0);
+    // D_i faces: M^T P M + alpha I + [has_next] P/dt^2
 #pragma unroll
-      for (int r = 0; r < B; ++r)
+    for (int a = 0; a < NF; ++a)
 #pragma unroll
-        for (int q = 0; q < B; ++q) A[r][q] = R(0);
+      for (int b = 0; b < NF; ++b) {
+        R s = R(0);
 #pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        A[q][q] = wall[q] ? R(1) : R(-1);
-        A[q][NF] = gcol[q];
-        A[NF][q] = -gcol[q];
-      }
-#pragma unroll
-      for (int q = 0; q < B; ++q) X[q][NF] = __ldg(in + (int64_t)q * M);
-      // coupling to the previous v-block (v_i): L = -I/dt on faces
-      if (i > 0) {
-#pragma unroll
-        for (int r = 0; r < NF; ++r) {
-          if (wall[r]) continue;
-#pragma unroll
-          for (int q = 0; q < NF; ++q) A[r][q] += idt * Wprev[r][q];
-          X[r][NF] += idt * zprev[r];
+        for (int t = 0; t < NF; ++t) s += Mc[t][a] * PM[t][b];
+        if (has_next) {
+          R pab = (a == b && !cg.wall[a] ? R(1) : R(0)) - cg.gcol[a] * cg.gcol[b] * isig;
+          s += pab * idt * idt;
         }
+        A[a][b] = s;
       }
-      // upper coupling to v_{i+1}: I/dt + J
 #pragma unroll
-      for (int r = 0; r < B; ++r)
-#pragma unroll
-        for (int q = 0; q < NF; ++q) X[r][q] = (r < NF) ? (J[r][q] + ((r == q && !wall[q]) ? idt : R(0))) : R(0);
-      ok &= dense_solve<R, B, C, false>(A, X, tinyv);
-      store(2 * i, X);
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        zprev[r] = X[r][NF];
-#pragma unroll
-        for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
-      }
+    for (int q = 0; q < NF; ++q) {
+      A[q][q] += cg.wall[q] ? R(1) : alpha;
+      A[q][NF] = cg.gcol[q];
+      A[NF][q] = -cg.gcol[q];
     }
-    // ================= v-block (rows R1[i], R2[i]; unknowns v_{i+1}, pbar) ====
-    {
-      R A[B][B], X[B][C];
-      const R alpha = (i < N - 1) ? kr : R(0);
+    A[NF][NF] = R(0);
+    // reduced rhs: yv + M^T c_i - [has_next] c_{i+1}/dt
+    R cn[NF];
+    if (has_next) {
+      R yun[B], yvn[B];
+      load_rows<DIM, PER, R>(asmb + (int64_t)(i + 1) * E * M + m, M, yun, yvn);
 #pragma unroll
-      for (int r = 0; r < B; ++r)
+      for (int q = 0; q < NF; ++q) cn[q] = yun[q];
+      projP(cn);
 #pragma unroll
-        for (int q = 0; q < B; ++q) A[r][q] = R(0);
+      for (int q = 0; q < NF; ++q) cn[q] += cg.gcol[q] * yun[NF] * isig;
+    } else {
 #pragma unroll
-      for (int q = 0; q < NF; ++q) {
-        A[q][q] = wall[q] ? R(1) : alpha;
-        A[q][NF] = gcol[q];
-        A[NF][q] = -gcol[q];
-      }
+      for (int q = 0; q < NF; ++q) cn[q] = R(0);
+    }
 #pragma unroll
-      for (int q = 0; q < B; ++q) X[q][NF] = __ldg(in + (int64_t)(B + q) * M);
-      // lower coupling to u_i: L = I/dt + J^T  ->  A -= L Wprev, rhs -= L zprev
+    for (int a = 0; a < NF; ++a) {
+      R s = yv[a];
 #pragma unroll
-      for (int r = 0; r < NF; ++r) {
-        if (wall[r]) continue;
+      for (int t = 0; t < NF; ++t) s += Mc[t][a] * cc[t];
+      X[a][NF] = cg.wall[a] ? R(0) : s - cn[a] * idt;
+    }
+    X[NF][NF] = yv[NF];
+    // lower coupling L_i = -(P M_i)^T / dt to dv_i:  A -= L Wprev, rhs -= L zprev
+    if (i > 0) {
 #pragma unroll
-        for (int q = 0; q < NF; ++q) {
+      for (int a = 0; a < NF; ++a) {
+#pragma unroll
+        for (int b = 0; b < NF; ++b) {
           R s = R(0);
 #pragma unroll
-          for (int t = 0; t < NF; ++t) {
-            R L = J[t][r] + ((t == r && !wall[r]) ? idt : R(0));
-            s += L * Wprev[t][q];
-          }
-          A[r][q] -= s;
+          for (int t = 0; t < NF; ++t) s += PM[t][a] * Wprev[t][b];
+          A[a][b] += s * idt;
         }
         R s = R(0);
 #pragma unroll
-        for (int t = 0; t < NF; ++t) {
-          R L = J[t][r] + ((t == r && !wall[r]) ? idt : R(0));
-          s += L * zprev[t];
-        }
-        X[r][NF] -= s;
+        for (int t = 0; t < NF; ++t) s += PM[t][a] * zprev[t];
+        X[a][NF] += s * idt;
       }
-      // upper coupling to u_{i+1}: -I/dt
+    }
+    // upper coupling U_i = -P M_{i+1} / dt (columns), load M_{i+1} first
+    R Mn[NF][NF];
+    if (has_next) {
+      frame_M<DIM, PER, R>(ix, c0, V, i + 1, cg, idt, Mn);
 #pragma unroll
-      for (int r = 0; r < B; ++r)
+      for (int b = 0; b < NF; ++b) {
+        R col[NF];
 #pragma unroll
-        for (int q = 0; q < NF; ++q)
-          X[r][q] = (i < N - 1 && r < NF && r == q && !wall[q]) ? -idt : R(0);
-      if (i < N - 1) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
-      else ok &= dense_solve<R, B, C, true>(A, X, tinyv);
-      store(2 * i + 1, X);
+        for (int a = 0; a < NF; ++a) col[a] = Mn[a][b];
+        projP(col);
 #pragma unroll
-      for (int r = 0; r < B; ++r) {
-        zprev[r] = X[r][NF];
+        for (int a = 0; a < B; ++a) X[a][b] = a < NF ? -col[a] * idt : R(0);
+      }
+    } else {
 #pragma unroll
-        for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
+      for (int a = 0; a < B; ++a)
+#pragma unroll
+        for (int b = 0; b < NF; ++b) X[a][b] = R(0);
+    }
+    if (alpha > R(0)) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
+    else ok &= dense_solve<R, B, C, true>(A, X, tinyv);
+    R* base = scratch + (int64_t)i * B * C * M + m;
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+#pragma unroll
+      for (int q = 0; q < C; ++q) base[(int64_t)(r * C + q) * M] = X[r][q];
+      zprev[r] = X[r][NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
+    }
+    if (has_next) {
+#pragma unroll
+      for (int a = 0; a < NF; ++a) {
+        cc[a] = cn[a];
+#pragma unroll
+        for (int b = 0; b < NF; ++b) Mc[a][b] = Mn[a][b];
       }
     }
   }
-  // ---- back substitution: x_b = z_b - W_b x_{b+1}[faces] ----
-  R xn[NF];
+
+  // ---- backward: dv (and dpbar) per pair, then du / dp of pair i+1 ----
+  // u-block of pair i needs dv_i (pair i-1) and dv_{i+1} (pair i)
+  auto u_delta = [&](int i, const R (&dvi)[NF], const R (&dvn)[NF]) {
+    R Mi[NF][NF];
+    frame_M<DIM, PER, R>(ix, c0, V, i, cg, idt, Mi);
+    R yu[B], yv[B];
+    load_rows<DIM, PER, R>(asmb + (int64_t)i * E * M + m, M, yu, yv);
+    R a[NF];
+    R ga = R(0);
 #pragma unroll
-  for (int q = 0; q < NF; ++q) xn[q] = R(0);
-  for (int blk = 2 * N - 1; blk >= 0; --blk) {
-    const R* base = scratch + (int64_t)blk * B * C * M + m;
+    for (int q = 0; q < NF; ++q) {
+      R s = yu[q] + dvi[q] * idt;
+#pragma unroll
+      for (int t = 0; t < NF; ++t) s -= Mi[q][t] * dvn[t];
+      a[q] = cg.wall[q] ? R(0) : s;
+      ga += cg.gcol[q] * a[q];
+    }
+    R dp = (ga - yu[NF]) * isig;
+    R* xo = xout + (int64_t)(2 * i) * B * M + m;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
+    xo[(int64_t)NF * M] = omega * dp;
+  };
+  R xn[NF];      // dv of pair i+1 (faces)
+  R xnn[NF];     // dv of pair i+2
+#pragma unroll
+  for (int q = 0; q < NF; ++q) xn[q] = xnn[q] = R(0);
+  for (int i = N - 1; i >= 0; --i) {
+    const R* base = scratch + (int64_t)i * B * C * M + m;
     R xb[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) {
@@ -494,11 +616,24 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
       for (int q = 0; q < NF; ++q) s -= base[(int64_t)(r * C + q) * M] * xn[q];
       xb[r] = s;
     }
-    R* xo = xout + (int64_t)blk * B * M + m;
+    R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
     for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
+    // u-block of pair i+1: dv_{i+1} = xb (this pair), dv_{i+2} = xn
+    if (i + 1 < N) {
+      R dvi[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
+      u_delta(i + 1, dvi, xn);
+    }
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];
+  }
+  {
+    R zero[NF];
+#pragma unroll
+    for (int q = 0; q < NF; ++q) zero[q] = R(0);
+    u_delta(0, zero, xn);   // dv_0 = 0 (pinned / frozen halo)
   }
   if (!ok) atomicExch(flag, 1);
 }
@@ -653,7 +788,7 @@ struct Nso : NsoBase {
       maxM = M > maxM ? M : maxM;
     }
     constexpr int B = Slots<DIM>::B, C = Slots<DIM>::C;
-    scratch = alloc((int64_t)2 * N * B * C * maxM);
+    scratch = alloc((int64_t)N * B * C * maxM);
     xout = alloc((int64_t)2 * N * B * maxM);
     asmb = alloc((int64_t)N * AsmLayout<DIM>::E * maxM);
     flag = (int*)mem.get(64);
