@@ -10,9 +10,10 @@ resident in HBM.  Default workload: BASELINE config 5 (3D 128^3 x 80 fp32,
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
     python bench.py --impl reference ...   # CPU oracle (port) on host cores
 
-Multi-GPU (N>1, torchrun): every rank solves its own replica of the workload
-("replicas", weak scaling) -- DESIGN.md §6 explains why the time-slab split
-is not yet the default.
+Multi-GPU (N>1, torchrun): the spacetime volume is split into N contiguous
+time slabs, one per rank (strong scaling: total work fixed); halos go over
+NCCL (torch.distributed P2P) before every residual / colour pass and ||f|| is
+an allreduce(max) -- paper_1608_01102_b200/slabs.py, DESIGN.md §6.
 """
 
 import argparse
@@ -151,7 +152,7 @@ def run_reference(args, w, rank, world):
     line = {
         "impl": "reference", "metric": "STFAS spacetime cell-updates/s (per V-cycle)", "value": val,
         "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "config_index": w.index, "cell_timesteps": w.cell_timesteps,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": val, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": sample},
@@ -196,21 +197,38 @@ def main():
     vstar = workloads.guide_velocity(w)
     v0 = workloads.initial_velocity(w)
     cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=w.levels)
-    state = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
-    hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
-    hier.set_guide(v0, vstar)
     stream = torch.cuda.current_stream()
+    slab = None
+    if world > 1:
+        from paper_1608_01102_b200 import slabs
+        slab, slab_states = slabs.build_lib_solver(spec, cfg, v0, vstar, [rank], world, w.N, w.dtype,
+                                                   comm=slabs.TorchComm())
+        state = slab_states[0]
+        hier = slab.E[0].hier
+        n_local = slab.E[0].Nl
+    else:
+        state = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
+        hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
+        hier.set_guide(v0, vstar)
+        n_local = w.N
+
+    def step():
+        if slab is not None:
+            slab.vcycle([state])
+            slab.gauge([state])
+        else:
+            hier.vcycle(state)
+            hier.gauge_fix(state)
 
     # inputs larger than L2 (126 MB) for configs >= 3; otherwise flush L2
     state_bytes = sum(t.numel() * t.element_size() for t in (*state.V, state.PB, *state.U, state.P))
-    guide_bytes = sum(t.numel() * t.element_size() for t in vstar)
+    guide_bytes = sum(t.numel() * t.element_size() for t in vstar) * n_local // w.N
     flush = None
     if state_bytes + guide_bytes < 4 * 126e6:
         flush = torch.empty(int(256e6) // 4, dtype=torch.float32, device="cuda")
 
     for _ in range(args.warmup):
-        hier.vcycle(state)
-        hier.gauge_fix(state)
+        step()
     torch.cuda.synchronize()
 
     # ---------------- timed region (device events) ----------------
@@ -228,8 +246,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        hier.vcycle(state)
-        hier.gauge_fix(state)
+        step()
         e1.record(stream)
         e1.synchronize()
         t_total += e0.elapsed_time(e1)
@@ -247,8 +264,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
-    ri, r2 = hier.residual_norms(state)
-    value = w.cell_timesteps * world / (ms / 1000.0)
+    if slab is not None:
+        ri, r2 = slab.norms([state])
+    else:
+        ri, r2 = hier.residual_norms(state)
+    value = w.cell_timesteps / (ms / 1000.0)
     hbm, peak_kind = peaks()
     esz = 4 if w.dtype == torch.float32 else 8
     # dominant kernel = the smoother kernel with the largest summed time; its
@@ -263,11 +283,11 @@ def main():
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                    "share_of_step": (v[0] / args.steps) / ms if ms else None} for k, v in kprof.items()}
     vc_bytes = vcycle_values_per_cts(w.dim, hier.levels) * esz * w.cell_timesteps
-    vc_gbs = vc_bytes / (ms / 1000.0) / 1e9
+    vc_gbs = vc_bytes / (ms / 1000.0) / 1e9 / world
 
     # ---------------- end to end through the public API ----------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and slab is None:
         pin = lambda t: t.detach().cpu().pin_memory()
         h_vs = [pin(t) for t in vstar]
         h_st = [pin(t) for t in (*state.V, state.PB, *state.U, state.P)]
@@ -286,8 +306,7 @@ def main():
             for d, h in zip(d_st, h_st):
                 d.copy_(h, non_blocking=True)
             hier.set_guide(v0, vstar)
-            hier.vcycle(state)
-            hier.gauge_fix(state)
+            step()
             for h, d in zip(out_h, d_st):
                 h.copy_(d, non_blocking=True)
             e1.record(stream)
@@ -312,11 +331,11 @@ def main():
             "metric": "STFAS spacetime cell-updates/s (per V-cycle)",
             "value": value, "unit": "cell-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "s_per_vcycle": ms / 1000.0,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32" if w.dtype == torch.float32 else "f64", "data": "synthetic",
             "config": {"workload": w.name, "config_index": w.index, "grid": f"{w.n}^{w.dim}", "frames": w.N,
                        "levels": hier.levels, "cell_timesteps": w.cell_timesteps,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": f"time-slabs x{world}" if world > 1 else "single",
                        "l2": "flushed" if flush is not None else "inputs larger than L2",
                        "residual_inf_after": ri},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": k_achieved, "peak": hbm,
@@ -324,7 +343,7 @@ def main():
                          "traffic": None, "avg_launch_ms": k_avg_ms, "launches": k_n,
                          "share_of_step": (k_ms / args.steps) / ms if ms else None},
             "smoother_kernels": kernels,
-            "vcycle_hbm": {"achieved": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
+            "vcycle_hbm": {"achieved_per_gpu": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
                            "algorithmic_bytes": vc_bytes},
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -142,6 +142,8 @@ typedef struct smk_nso_params {
   int nu1, nu2;   /* pre/post sweeps (2, 2) */
   int n_coarse;   /* coarsest sweeps (10) */
   int color_mod;  /* colouring modulus per axis (2: 4/8 colours) */
+  int t0;         /* time-slab mode: global index of local pair 0 (0 otherwise) */
+  int n_total;    /* time-slab mode: global pair count (0 = n_frames) */
 } smk_nso_params;
 
 /* Spacetime state (pair index i = 0..N-1): V[i]=v_{i+1}, PB[i]=pbar_{i+1},
@@ -197,6 +199,23 @@ int smk_nso_gauge_fix(smk_nso* h, const smk_state* s, void* stream);
  * SMK_NONCONVERGENCE if the budget is exhausted. */
 int smk_nso_solve(smk_nso* h, const smk_state* s, double eps, int relative, int cycle_budget, int* cycles,
                   double* hist, void* stream);
+
+/* ---- time-slab (multi-GPU) per-level operations ----
+ * The caller owns the level's state (n_frames local pairs) and passes the
+ * slab halos explicitly: vprev = v at the frame before local pair 0 (the left
+ * neighbour's last V frame, or the pinned v0 on the first slab), unext = the
+ * right neighbour's first U frame (NULL on the last slab), vs = the level's
+ * guide with n_frames + 1 frames (v*_{t0} .. v*_{t0+n_frames}).  The smoother's
+ * time line is cut at the slab boundary (neighbour frames frozen). */
+int smk_nso_n_colors(const smk_nso* h);
+int smk_nso_level_residual(smk_nso* h, int level, const smk_state* s, const void* const vprev[],
+                           const void* const unext[], const void* const vs[], const smk_residual* rhs,
+                           const smk_residual* out, void* stream);
+int smk_nso_level_color_pass(smk_nso* h, int level, int colour, const smk_state* s, const void* const vprev[],
+                             const void* const unext[], const void* const vs[], const smk_residual* rhs,
+                             void* stream);
+/* y = a * x + b * y over n elements (state algebra of the slab V-cycle) */
+int smk_axpby(int dtype, void* y, const void* x, double a, double b, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

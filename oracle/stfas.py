@@ -88,10 +88,21 @@ class Problem:
     vstar: tuple       # (N, face) stacks: v*_0 .. v*_{N-1}
     omega: float = 0.8
     colors: int = 2    # colouring modulus per axis (2 -> 2^d colours)
+    # time-slab mode: local pairs t0 .. t0+n_pairs-1 of Ng;
+    # v0 is the left halo, unext the right halo u_{t0+n_pairs}, vstar holds
+    # n_pairs + 1 frames (v*_{t0} .. v*_{t0+n_pairs})
+    t0: int = 0
+    Ng: int = 0
+    n_pairs: int = 0
+    unext: tuple = None
 
     @property
     def N(self):
-        return self.vstar[0].shape[0]
+        return self.n_pairs if self.n_pairs else self.vstar[0].shape[0]
+
+    @property
+    def N_global(self):
+        return self.Ng if self.Ng else self.N
 
     @property
     def kr(self):
@@ -124,11 +135,17 @@ def kkt_residual(pb, st):
     R3 = tuple((v - vp) / dt + a - u + q
                for v, vp, a, u, q in zip(V, vprev, adv, U, gp))
     R4 = ops.div(g, U)
-    kmask = (np.arange(N) < N - 1).astype(np.float64)
+    kmask = (pb.t0 + np.arange(N) < pb.N_global - 1).astype(np.float64)
     kmask = kmask.reshape((N,) + (1,) * g.dim)
-    unext = tuple(np.concatenate([u[1:], np.zeros_like(u[:1])], axis=0) for u in U)
-    vs_next = tuple(np.concatenate([s[1:], np.zeros_like(s[:1])], axis=0)
-                    for s in pb.vstar)
+    if pb.unext is not None:
+        unext = tuple(np.concatenate([u[1:], h[None]], axis=0) for u, h in zip(U, pb.unext))
+    else:
+        unext = tuple(np.concatenate([u[1:], np.zeros_like(u[:1])], axis=0) for u in U)
+    if pb.vstar[0].shape[0] == N + 1:
+        vs_next = tuple(s[1:] for s in pb.vstar)
+    else:
+        vs_next = tuple(np.concatenate([s[1:], np.zeros_like(s[:1])], axis=0)
+                        for s in pb.vstar)
     jt = ops.jac_T_apply(g, V, U)
     gpb = ops.grad(g, st.PB)
     R1 = tuple(kmask * (pb.kr * (v - s) - un / dt) + u / dt + j + q
@@ -263,7 +280,7 @@ def assemble_line(pb, slots, J):
         D[:, bu, :nf, nf] = gc
         D[:, bu, nf, :nf] = -gc           # div row = -grad^T
         # v-block: rows R1[i] + R2[i]; unknowns v_{i+1}, pbar_{i+1}
-        alpha = pb.kr if i < N - 1 else 0.0
+        alpha = pb.kr if pb.t0 + i < pb.N_global - 1 else 0.0
         D[:, bv, :nf, :nf] = alpha * eye
         D[:, bv, :nf, nf] = gc
         D[:, bv, nf, :nf] = -gc

@@ -35,7 +35,7 @@ class smk_nso_params(ctypes.Structure):
     _fields_ = [("n_frames", ctypes.c_int), ("n_levels", ctypes.c_int), ("dt", ctypes.c_double),
                 ("K", ctypes.c_double), ("r", ctypes.c_double), ("omega", ctypes.c_double),
                 ("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("n_coarse", ctypes.c_int),
-                ("color_mod", ctypes.c_int)]
+                ("color_mod", ctypes.c_int), ("t0", ctypes.c_int), ("n_total", ctypes.c_int)]
 
 
 VP3 = ctypes.c_void_p * 3
@@ -99,6 +99,10 @@ SIGNATURES = {
     "smk_nso_residual_norms": (I, [P, PS, PD, PD, P]),
     "smk_nso_gauge_fix": (I, [P, PS, P]),
     "smk_nso_solve": (I, [P, PS, D, I, I, PI, PD, P]),
+    "smk_nso_n_colors": (I, [P]),
+    "smk_nso_level_residual": (I, [P, I, PS, P, P, P, PR, PR, P]),
+    "smk_nso_level_color_pass": (I, [P, I, I, PS, P, P, P, PR, P]),
+    "smk_axpby": (I, [I, P, P, D, D, I64, P]),
 }
 
 _lib = None

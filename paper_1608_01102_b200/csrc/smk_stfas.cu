@@ -56,11 +56,17 @@ template <int DIM, bool PER, class R>
 struct KktCtx {
   Ix<DIM, PER> ix;
   R c0, h, dt, kr;
-  int N;
+  int N;           // local pairs (this slab)
+  int t0, Ng;      // global index of local pair 0, global pair count
   int64_t nf[3], nc;
   Face3<R> V, U, v0, vs;
+  Face3<R> un;     // right halo u_{t0+N} (slab mode; unused when t0+N == Ng)
   const R* P;
   const R* PB;
+
+  // K-term / u_{i+1} present for local pair i (global i < Ng-1)
+  __device__ __forceinline__ bool inner(int i) const { return t0 + i < Ng - 1; }
+  __device__ __forceinline__ Face3<R> u_next(int i) const { return i < N - 1 ? frame_of(U, i + 1, nf) : un; }
 
   __device__ __forceinline__ R grad_at(const R* p, int k, const int f[3]) const {
     if (ix.wall(k, f)) return R(0);
@@ -98,10 +104,10 @@ struct KktCtx {
     Face3<R> Ui = frame_of(U, i, nf);
     int64_t o = ix.face_off(j, f[0], f[1], f[2]);
     R t1 = R(0);
-    if (i < N - 1) {
+    if (inner(i)) {
       R s = vs.c[j][(int64_t)(i + 1) * nf[j] + o];
-      R un = U.c[j][(int64_t)(i + 1) * nf[j] + o];
-      t1 = kr * (Vi.c[j][o] - s) - un / dt;
+      R unv = u_next(i).c[j][o];
+      t1 = kr * (Vi.c[j][o] - s) - unv / dt;
     }
     MemField<DIM, PER, R> Av{ix, Vi}, Au{ix, Ui};
     R jt = JT_at<DIM, PER, R>(ix, c0, j, f, Av, Au);
@@ -318,8 +324,8 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
     Face3<R> Vi = frame_of(cx.V, i, cx.nf);
     Face3<R> Ui = frame_of(cx.U, i, cx.nf);
     Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
-    const bool inner = i < cx.N - 1;
-    Face3<R> Un = inner ? frame_of(cx.U, i + 1, cx.nf) : Vi;
+    const bool inner = cx.inner(i);
+    Face3<R> Un = inner ? cx.u_next(i) : Vi;
     Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Vi;
     NbrField<DIM, PER, R> VC(ix, c, Vi), UC(ix, c, Ui);
     const R* Pi = cx.P + (int64_t)i * cx.nc;
@@ -415,7 +421,7 @@ __device__ __forceinline__ void frame_M(const Ix<DIM, PER>& ix, R c0, const Face
 }
 
 template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, Face3<R> V,
+__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, int t0, int Ng, Face3<R> V,
                                                   int o0, int o1, int o2, int mod, int m0, int m1, int m2, R omega,
                                                   const R* __restrict__ asmb, R* __restrict__ scratch,
                                                   R* __restrict__ xout, int* flag) {
@@ -478,7 +484,7 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
       for (int a = 0; a < NF; ++a) PM[a][b] = col[a];
     }
     R A[B][B], X[B][C];
-    const R alpha = (i < N - 1) ? kr : R(0);
+    const R alpha = (t0 + i < Ng - 1) ? kr : R(0);
     // D_i faces: M^T P M + alpha I + [has_next] P/dt^2
 #pragma unroll
     for (int a = 0; a < NF; ++a)
@@ -699,6 +705,13 @@ struct NsoBase {
   virtual int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) = 0;
   virtual int gauge(const smk_state* s, cudaStream_t st) = 0;
   virtual int levels() const = 0;
+  virtual int ncolors() const = 0;
+  virtual int level_residual(int l, const smk_state* s, const void* const vprev[], const void* const unext[],
+                             const void* const vs[], const smk_residual* rhs, const smk_residual* out,
+                             cudaStream_t st) = 0;
+  virtual int level_color_pass(int l, int colour, const smk_state* s, const void* const vprev[],
+                               const void* const unext[], const void* const vs[], const smk_residual* rhs,
+                               cudaStream_t st) = 0;
   virtual int profile(int enable) = 0;
   virtual int profile_read(int kind, double* ms, long long* launches, long long* cells) = 0;
   virtual int64_t bytes() const = 0;
@@ -830,9 +843,18 @@ struct Nso : NsoBase {
   }
   int64_t bytes() const override { return nbytes; }
 
+  // slab halos for the next residual / colour pass (set by the level API)
+  const void* halo_vprev[3] = {nullptr, nullptr, nullptr};
+  const void* halo_unext[3] = {nullptr, nullptr, nullptr};
+  const void* halo_vs[3] = {nullptr, nullptr, nullptr};
+  bool use_halo = false;
+
   KktCtx<DIM, PER, R> ctx(int l, const StP<R>& s) const {
     const Level<R>& L = lv[l];
     KktCtx<DIM, PER, R> c{Ix<DIM, PER>(L.g)};
+    c.t0 = prm.t0;
+    c.Ng = prm.n_total > 0 ? prm.n_total : prm.n_frames;
+    for (int k = 0; k < 3; ++k) c.un.c[k] = use_halo ? (const R*)halo_unext[k] : nullptr;
     c.c0 = (R)(0.5 / L.g.h);
     c.h = (R)L.g.h;
     c.dt = (R)prm.dt;
@@ -843,8 +865,8 @@ struct Nso : NsoBase {
     for (int k = 0; k < 3; ++k) {
       c.V.c[k] = s.V[k];
       c.U.c[k] = s.U[k];
-      c.v0.c[k] = l == 0 ? (const R*)top_v0[k] : L.v0[k];
-      c.vs.c[k] = l == 0 ? (const R*)top_vs[k] : L.vs[k];
+      c.v0.c[k] = use_halo ? (const R*)halo_vprev[k] : (l == 0 ? (const R*)top_v0[k] : L.v0[k]);
+      c.vs.c[k] = use_halo ? (const R*)halo_vs[k] : (l == 0 ? (const R*)top_vs[k] : L.vs[k]);
     }
     c.P = s.P;
     c.PB = s.PB;
@@ -872,42 +894,50 @@ struct Nso : NsoBase {
     k_kkt_cells<DIM, PER, R><<<grid_for(nca, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
   }
 
+  int n_colors() const {
+    int ncol = 1;
+    for (int a = 0; a < DIM; ++a) ncol *= prm.color_mod;
+    return ncol;
+  }
+
   void sweep(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
+    for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
+  }
+
+  void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
     const Level<R>& L = lv[l];
     const int mod = prm.color_mod;
-    int ncol = 1;
-    for (int a = 0; a < DIM; ++a) ncol *= mod;
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     Ix<DIM, PER> ix(L.g);
-    for (int col = 0; col < ncol; ++col) {
-      int o[3] = {0, 0, 0}, mm[3] = {1, 1, 1};
-      int cc = col;
-      for (int a = 0; a < DIM; ++a) {
-        o[a] = cc % mod;
-        cc /= mod;
-        mm[a] = (L.g.n[a] - o[a] + mod - 1) / mod;
-        if (mm[a] < 0) mm[a] = 0;
-      }
-      int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
-      if (M == 0) continue;
-      int64_t tot = (int64_t)prm.n_frames * M;
-      prof_begin(0, M, st);
-      k_scgs_assemble<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod,
-                                                                       mm[0], mm[1], mm[2], asmb); count_launch();
-      prof_end(0, st);
-      // latency-bound recursion: spread small colours over all SMs
-      int tpb = M >= 148 * 128 ? 128 : 32;
-      prof_begin(1, M, st);
-      k_scgs_line<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(
-          ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, c.V, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-          (R)prm.omega, asmb, scratch, xout, flag); count_launch();
-      prof_end(1, st);
-      prof_begin(2, M, st);
-      k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
-                                                                     mm[1], mm[2], xout); count_launch();
-      prof_end(2, st);
+    int o[3] = {0, 0, 0}, mm[3] = {1, 1, 1};
+    int cc = col;
+    for (int a = 0; a < DIM; ++a) {
+      o[a] = cc % mod;
+      cc /= mod;
+      mm[a] = (L.g.n[a] - o[a] + mod - 1) / mod;
+      if (mm[a] < 0) mm[a] = 0;
     }
+    int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
+    if (M == 0) return;
+    int64_t tot = (int64_t)prm.n_frames * M;
+    prof_begin(0, M, st);
+    k_scgs_assemble<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod,
+                                                                     mm[0], mm[1], mm[2], asmb); count_launch();
+    prof_end(0, st);
+    // latency-bound recursion: spread small colours over all SMs
+    int tpb = M >= 148 * 128 ? 128 : 32;
+    prof_begin(1, M, st);
+    k_scgs_line<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(
+        ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, c.t0, c.Ng, c.V, o[0], o[1], o[2], mod, mm[0],
+        mm[1], mm[2],
+        (R)prm.omega, asmb, scratch, xout, flag); count_launch();
+    prof_end(1, st);
+    prof_begin(2, M, st);
+    k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
+                                                                   mm[1], mm[2], xout); count_launch();
+    prof_end(2, st);
+
   }
 
   void restrict_state(int l, const StP<R>& fine, const StP<R>& coarse, cudaStream_t st) {
@@ -1071,6 +1101,44 @@ struct Nso : NsoBase {
     return check_flag(st);
   }
 
+  // ---- slab (per-level) API: caller owns the level's state and halos ----
+  void set_halo(const void* const vprev[], const void* const unext[], const void* const vs[]) {
+    for (int k = 0; k < 3; ++k) {
+      halo_vprev[k] = k < DIM ? vprev[k] : nullptr;
+      halo_unext[k] = (k < DIM && unext) ? unext[k] : nullptr;
+      halo_vs[k] = k < DIM ? vs[k] : nullptr;
+    }
+    use_halo = true;
+  }
+  static ResP<R> res_from_api(const smk_residual* r) {
+    ResP<R> o{};
+    if (!r) return o;
+    for (int k = 0; k < 3; ++k) { o.R1[k] = (R*)r->R1[k]; o.R3[k] = (R*)r->R3[k]; }
+    o.R2 = (R*)r->R2; o.R4 = (R*)r->R4;
+    return o;
+  }
+  int ncolors() const override { return n_colors(); }
+  int level_residual(int l, const smk_state* s, const void* const vprev[], const void* const unext[],
+                     const void* const vs[], const smk_residual* rhs, const smk_residual* out,
+                     cudaStream_t st) override {
+    if (l < 0 || l >= (int)lv.size()) { set_error("bad level"); return SMK_ERR_ARG; }
+    set_halo(vprev, unext, vs);
+    ResP<R> r = res_from_api(rhs);
+    residual(l, from_api(s), rhs ? &r : nullptr, res_from_api(out), st);
+    use_halo = false;
+    return cuda_check("nso_level_residual");
+  }
+  int level_color_pass(int l, int colour, const smk_state* s, const void* const vprev[], const void* const unext[],
+                       const void* const vs[], const smk_residual* rhs, cudaStream_t st) override {
+    if (l < 0 || l >= (int)lv.size()) { set_error("bad level"); return SMK_ERR_ARG; }
+    if (colour < 0 || colour >= n_colors()) { set_error("bad colour"); return SMK_ERR_ARG; }
+    set_halo(vprev, unext, vs);
+    ResP<R> r = res_from_api(rhs);
+    color_pass(l, colour, from_api(s), rhs ? &r : nullptr, st);
+    use_halo = false;
+    return cuda_check("nso_level_color_pass");
+  }
+
   // standalone entry points (level-0 only)
   int residual_api(const smk_state* s, const smk_residual* rhs, const smk_residual* out, cudaStream_t st) {
     StP<R> top = from_api(s);
@@ -1108,6 +1176,10 @@ struct smk_nso {
 
 static int check_params(const smk_nso_params* p) {
   if (!p) { set_error("null params"); return SMK_ERR_ARG; }
+  if (p->t0 < 0 || p->n_total < 0 || (p->n_total > 0 && p->t0 + p->n_frames > p->n_total)) {
+    set_error("bad slab range (t0, n_total)");
+    return SMK_ERR_ARG;
+  }
   if (p->n_frames < 1) { set_error("n_frames must be >= 1"); return SMK_ERR_ARG; }
   if (!(p->dt > 0) || !(p->r > 0) || !(p->K >= 0)) { set_error("dt, r must be positive, K >= 0"); return SMK_ERR_ARG; }
   if (p->color_mod < 2) { set_error("color_mod must be >= 2"); return SMK_ERR_ARG; }
@@ -1153,6 +1225,30 @@ void smk_nso_destroy(smk_nso* h) {
 }
 
 int smk_nso_levels(const smk_nso* h) { return h ? h->impl->levels() : 0; }
+int smk_nso_n_colors(const smk_nso* h) { return h ? h->impl->ncolors() : 0; }
+
+int smk_nso_level_residual(smk_nso* h, int level, const smk_state* s, const void* const vprev[],
+                           const void* const unext[], const void* const vs[], const smk_residual* rhs,
+                           const smk_residual* out, void* stream) {
+  if (!h || !s || !out || !vprev || !vs) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->level_residual(level, s, vprev, unext, vs, rhs, out, (cudaStream_t)stream);
+}
+
+int smk_nso_level_color_pass(smk_nso* h, int level, int colour, const smk_state* s, const void* const vprev[],
+                             const void* const unext[], const void* const vs[], const smk_residual* rhs,
+                             void* stream) {
+  if (!h || !s || !vprev || !vs) { set_error("null argument"); return SMK_ERR_ARG; }
+  int rc = h->impl->level_color_pass(level, colour, s, vprev, unext, vs, rhs, (cudaStream_t)stream);
+  return rc;
+}
+
+int smk_axpby(int dtype, void* y, const void* x, double a, double b, int64_t n, void* stream) {
+  if (dtype == SMK_F64) axpby<double>((double*)y, (const double*)x, a, b, n, (cudaStream_t)stream);
+  else if (dtype == SMK_F32) axpby<float>((float*)y, (const float*)x, a, b, n, (cudaStream_t)stream);
+  else { set_error("bad dtype"); return SMK_ERR_ARG; }
+  count_launch();
+  return cuda_check("smk_axpby");
+}
 
 int smk_nso_profile(smk_nso* h, int enable) {
   if (!h) { set_error("null handle"); return SMK_ERR_ARG; }

@@ -37,8 +37,10 @@ class StfasConfig:
     color_mod: int = 2          # 4 colours (2D) / 8 colours (3D)
     n_levels: int = 99          # clipped to the grid's coarsening chain
 
-    def params(self, N):
+    def params(self, N, t0=0, n_total=0):
         p = _lib.smk_nso_params()
+        p.t0 = int(t0)
+        p.n_total = int(n_total)
         p.n_frames = int(N)
         p.n_levels = int(self.n_levels)
         p.dt = float(self.dt)
@@ -207,13 +209,13 @@ def prolong(spec_coarse, x):
 class StfasHierarchy:
     """Device-resident level hierarchy over libsmk's handle."""
 
-    def __init__(self, spec, cfg, N, dtype=torch.float64):
+    def __init__(self, spec, cfg, N, dtype=torch.float64, t0=0, n_total=0):
         _dev.require_device()
         self.spec, self.cfg, self.N, self.dtype = spec, cfg, int(N), dtype
         L = _lib.load()
         self._L = L
         self._g = _dev.grid(spec, dtype)
-        self._p = cfg.params(N)
+        self._p = cfg.params(N, t0, n_total)
         h = L.smk_nso_create(ctypes.byref(self._g), ctypes.byref(self._p))
         if not h:
             _lib.check(_lib.SMK_ERR_CUDA if "alloc" in _lib.last_error() else _lib.SMK_ERR_ARG, "nso_create")

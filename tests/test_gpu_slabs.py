@@ -1,0 +1,77 @@
+"""Time-slab solver on B200 (libsmk engine): a single slab reproduces the
+C++ hierarchy's V-cycle, two in-process slabs reproduce the oracle's slab
+iterates and converge to the single-slab solution."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import stfas
+from problems import make_problem
+from slab_oracle import build_oracle_solver
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(pb, slab_ids, n_slabs, n_levels):
+    from paper_1608_01102_b200 import nso
+    from paper_1608_01102_b200.fields import GridSpec
+    from paper_1608_01102_b200.slabs import build_lib_solver
+    g = pb.g
+    spec = GridSpec(g.dim, g.res, g.h, g.boundary)
+    cfg = nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, n_levels=n_levels)
+    return spec, cfg, build_lib_solver(spec, cfg, pb.v0, pb.vstar, slab_ids, n_slabs, pb.N)
+
+
+def flat_dev(st):
+    V, PB, U, P = st.numpy()
+    return np.concatenate([a.ravel() for a in V + (PB,) + U + (P,)])
+
+
+def flat_np(st):
+    return np.concatenate([a.ravel() for a in st.V + (st.PB,) + st.U + (st.P,)])
+
+
+def test_single_slab_equals_hierarchy_vcycle():
+    from paper_1608_01102_b200 import nso
+    pb = make_problem(2, n=16, N=6, seed=201)
+    spec, cfg, (solver, states) = setup(pb, [0], 1, 3)
+    solver.vcycle(states)
+    s = nso.SpacetimeState.zeros(spec, pb.N)
+    hier = nso.StfasHierarchy(spec, cfg, pb.N)
+    hier.set_guide(pb.v0, pb.vstar)
+    hier.vcycle(s)
+    a, b = flat_dev(states[0]), flat_dev(s)
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_two_slabs_match_oracle_slabs(dim):
+    n = 16 if dim == 2 else 8
+    pb = make_problem(dim, n=n, N=6, seed=202)
+    spec, cfg, (solver, states) = setup(pb, [0, 1], 2, 2)
+    osolver, ostates = build_oracle_solver(pb, 2, [0, 1], 2)
+    for _ in range(2):
+        solver.vcycle(states)
+        solver.gauge(states)
+        osolver.vcycle(ostates)
+        osolver.gauge(ostates)
+    for d, o in zip(states, ostates):
+        a, b = flat_dev(d), flat_np(o)
+        assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+
+
+def test_four_slabs_converge_to_single_slab_solution():
+    pb = make_problem(2, n=16, N=8, seed=203)
+    _, _, (one, s1) = setup(pb, [0], 1, 3)
+    one.solve(s1, eps=1e-10, cycle_budget=80)
+    _, _, (four, s4) = setup(pb, [0, 1, 2, 3], 4, 3)
+    h4 = four.solve(s4, eps=1e-10, cycle_budget=120)
+    assert h4[-1][1] <= 1e-10
+    a = flat_dev(s1[0])
+    V = [np.concatenate([st.numpy()[0][k] for st in s4]) for k in range(2)]
+    U = [np.concatenate([st.numpy()[2][k] for st in s4]) for k in range(2)]
+    V1, _, U1, _ = s1[0].numpy()
+    scale = max(np.max(np.abs(x)) for x in V1 + U1)
+    err = max(np.max(np.abs(x - y)) for x, y in zip(V + U, list(V1) + list(U1)))
+    assert err <= 1e-8 * scale
