@@ -271,13 +271,12 @@ def main():
     value = w.cell_timesteps / (ms / 1000.0)
     hbm, peak_kind = peaks()
     esz = 4 if w.dtype == torch.float32 else 8
-    # dominant kernel = the smoother kernel with the largest summed time; its
-    # algorithmic bytes are its share of the sweep traffic:
-    # (2s + g) values per cell-timestep per sweep, split evenly over the
-    # assemble / line / apply kernels of each colour pass
-    kname = max(kprof, key=lambda k: kprof[k][0])
+    # dominant kernel = the colour-pass forward kernel k_scgs_fwd; its
+    # algorithmic bytes are the sweep traffic of the cells it updates
+    # (SURVEY §8d): (2s + g) values per colour cell-timestep
+    kname = "k_scgs_fwd"
     k_ms, k_n, k_cells = kprof[kname]
-    k_bytes = k_cells * sweep_values(w.dim) * esz / 3.0
+    k_bytes = k_cells * sweep_values(w.dim) * esz
     k_avg_ms = k_ms / max(k_n, 1)
     k_achieved = (k_bytes / max(k_n, 1)) / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,

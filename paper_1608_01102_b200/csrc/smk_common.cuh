@@ -190,6 +190,85 @@ struct NbrField {
 };
 
 // ---------------------------------------------------------------------------
+// One cell's position with cheap neighbour addressing inside a frame.
+// Neumann: a face / cell read at a compile-time offset d from c is in range
+// iff, per axis a, (d_a == -1 -> c_a >= 1) and (d_a == +1 across, or +2 along
+// the face's own axis -> c_a <= n_a - 2); out-of-range reads are 0, like
+// Ix::face / Ix::cell.  Offsets are 32-bit within a frame (a 129*128*128
+// face frame is 2.1M elements); the frame base pointer carries the rest.
+// Periodic: wrapped through Ix (cold path, not used by the benchmarks).
+// ---------------------------------------------------------------------------
+template <int DIM, bool PER>
+struct Loc {
+  int c[3];
+  bool lo[3], hi[3];
+  int of[2 * DIM];   // offsets of the cell's own faces (q = 2k + side)
+  int co;            // cell offset
+  __device__ __forceinline__ Loc(const Ix<DIM, PER>& ix, const int cc[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      c[a] = cc[a];
+      lo[a] = cc[a] >= 1;
+      hi[a] = cc[a] <= ix.n(a) - 2;
+    }
+    co = (int)ix.cell_off(c[0], c[1], c[2]);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        int f[3] = {c[0], c[1], c[2]};
+        f[k] += s;
+        if (PER && f[k] >= ix.n(k)) f[k] -= ix.n(k);
+        of[2 * k + s] = (int)ix.face_off(k, f[0], f[1], f[2]);
+      }
+  }
+  // stride of face component k along axis a (axis 2 / the 2D last axis: 1)
+  __device__ __forceinline__ static int fstride(const Ix<DIM, PER>& ix, int k, int a) {
+    if (a == 2) return 1;
+    if (DIM == 2) return a == 0 ? ix.fe(k, 1) : 1;
+    return a == 0 ? ix.fe(k, 1) * ix.fe(k, 2) : ix.fe(k, 2);
+  }
+  __device__ __forceinline__ static int cstride(const Ix<DIM, PER>& ix, int a) {
+    if (a == 2) return 1;
+    if (DIM == 2) return a == 0 ? ix.n1 : 1;
+    return a == 0 ? ix.n1 * ix.n2 : ix.n2;
+  }
+  __device__ __forceinline__ bool ok(int a, int d, int up) const {
+    return d < 0 ? lo[a] : (d >= up ? hi[a] : true);
+  }
+  template <class R>
+  __device__ __forceinline__ R face(const Ix<DIM, PER>& ix, const R* __restrict__ p, int k, int d0, int d1,
+                                    int d2) const {
+    if (PER) return ix.face(p, k, c[0] + d0, c[1] + d1, c[2] + d2);
+    bool v = ok(0, d0, k == 0 ? 2 : 1) && ok(1, d1, k == 1 ? 2 : 1) && (DIM == 2 || ok(2, d2, k == 2 ? 2 : 1));
+    int o = of[2 * k] + d0 * fstride(ix, k, 0) + d1 * fstride(ix, k, 1) + (DIM == 3 ? d2 : 0);
+    return v ? __ldg(p + o) : R(0);
+  }
+  template <class R>
+  __device__ __forceinline__ R cell(const Ix<DIM, PER>& ix, const R* __restrict__ p, int d0, int d1, int d2) const {
+    if (PER) return ix.cell(p, c[0] + d0, c[1] + d1, c[2] + d2);
+    bool v = ok(0, d0, 1) && ok(1, d1, 1) && (DIM == 2 || ok(2, d2, 1));
+    int o = co + d0 * cstride(ix, 0) + d1 * cstride(ix, 1) + (DIM == 3 ? d2 : 0);
+    return v ? __ldg(p + o) : R(0);
+  }
+};
+
+// register cache of one face field around a cell (NbrSlots layout), loaded
+// through Loc; slots a stencil does not use are dead and never loaded
+template <int DIM, bool PER, class R>
+__device__ __forceinline__ void load_nbr(const Ix<DIM, PER>& ix, const Loc<DIM, PER>& L, const Face3<R>& f,
+                                         R (&val)[DIM][NbrSlots<DIM>::NB]) {
+#pragma unroll
+  for (int a = 0; a < DIM; ++a)
+#pragma unroll
+    for (int sl = 0; sl < NbrSlots<DIM>::NB; ++sl) {
+      int d[3];
+      NbrSlots<DIM>::offset(a, sl, d);
+      val[a][sl] = L.face(ix, f.c[a], a, d[0], d[1], d[2]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Closed-form S(v,w)_J, T(v,u)_J at the cell's own J-face f = c + SD e_J from
 // register caches (same arithmetic as S_at / Tadj_at, compile-time slots).
 // Valid for non-wall faces (Neumann: both cells of the face exist).

@@ -56,6 +56,7 @@ template <int DIM, bool PER, class R>
 struct KktCtx {
   Ix<DIM, PER> ix;
   R c0, h, dt, kr;
+  R ih, idt;       // 1/h, 1/dt (host-rounded; exact for h = 2^-k)
   int N;           // local pairs (this slab)
   int t0, Ng;      // global index of local pair 0, global pair count
   int64_t nf[3], nc;
@@ -67,89 +68,130 @@ struct KktCtx {
   // K-term / u_{i+1} present for local pair i (global i < Ng-1)
   __device__ __forceinline__ bool inner(int i) const { return t0 + i < Ng - 1; }
   __device__ __forceinline__ Face3<R> u_next(int i) const { return i < N - 1 ? frame_of(U, i + 1, nf) : un; }
-
-  __device__ __forceinline__ R grad_at(const R* p, int k, const int f[3]) const {
-    if (ix.wall(k, f)) return R(0);
-    int lo[3];
-    shift((int*)f, k, -1, lo);
-    return (ix.cell(p, f[0], f[1], f[2]) - ix.cell(p, lo[0], lo[1], lo[2])) / h;
-  }
-  __device__ __forceinline__ R div_at(const Face3<R>& v, const int c[3]) const {
-    R acc = R(0);
-#pragma unroll
-    for (int k = 0; k < DIM; ++k) {
-      int hi[3];
-      shift((int*)c, k, 1, hi);
-      R d = (ix.face(v.c[k], k, hi[0], hi[1], hi[2]) - v.c[k][ix.face_off(k, c[0], c[1], c[2])]) / h;
-      acc = (k == 0) ? d : acc + d;
-    }
-    return acc;
-  }
-  // R3[i] at j-face f
-  __device__ R r3(int i, int j, const int f[3]) const {
-    if (ix.wall(j, f)) return R(0);
-    Face3<R> Vi = frame_of(V, i, nf);
-    Face3<R> Vp = i == 0 ? v0 : frame_of(V, i - 1, nf);
-    int64_t o = ix.face_off(j, f[0], f[1], f[2]);
-    MemField<DIM, PER, R> A{ix, Vi};
-    R adv = S_at<DIM, PER, R>(ix, c0, j, f, A, A);
-    R u = U.c[j][(int64_t)i * nf[j] + o];
-    R q = grad_at(P + (int64_t)i * nc, j, f);
-    return (((Vi.c[j][o] - Vp.c[j][o]) / dt + adv) - u) + q;
-  }
-  // R1[i] at j-face f
-  __device__ R r1(int i, int j, const int f[3]) const {
-    if (ix.wall(j, f)) return R(0);
-    Face3<R> Vi = frame_of(V, i, nf);
-    Face3<R> Ui = frame_of(U, i, nf);
-    int64_t o = ix.face_off(j, f[0], f[1], f[2]);
-    R t1 = R(0);
-    if (inner(i)) {
-      R s = vs.c[j][(int64_t)(i + 1) * nf[j] + o];
-      R unv = u_next(i).c[j][o];
-      t1 = kr * (Vi.c[j][o] - s) - unv / dt;
-    }
-    MemField<DIM, PER, R> Av{ix, Vi}, Au{ix, Ui};
-    R jt = JT_at<DIM, PER, R>(ix, c0, j, f, Av, Au);
-    R q = grad_at(PB + (int64_t)i * nc, j, f);
-    return ((t1 + Ui.c[j][o] / dt) + jt) + q;
-  }
-  __device__ R r2(int i, const int c[3]) const { return div_at(frame_of(V, i, nf), c); }
-  __device__ R r4(int i, const int c[3]) const { return div_at(frame_of(U, i, nf), c); }
 };
 
-template <int DIM, bool PER, class R>
-__global__ void k_kkt_faces(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
-  const int j = blockIdx.y;
-  const int64_t nf = cx.nf[j];
-  SMK_GRID_STRIDE(t, (int64_t)cx.N * nf) {
-    int i = (int)(t / nf);
-    int f[3];
-    cx.ix.face_idx(j, t - (int64_t)i * nf, f);
-    R a = cx.r1(i, j, f), b = cx.r3(i, j, f);
-    if (has_rhs) {
-      a -= rhs.R1[j][t];
-      b -= rhs.R3[j][t];
+// ---------------------------------------------------------------------------
+// Eq. 8 rows of one cell, shared by the residual kernel and the smoother.
+//
+// f - rhs of pair i at the cell's own faces q = 2j + sd (sd = 0 always, sd = 1
+// when BOTH) and at the cell: yu = (R3, R4) rows, yv = (R1, R2) rows.  Inputs
+// are register caches of V_i (VC) and U_i (UC) around the cell and V_{i-1} at
+// the own faces (vp).  Wall rows (Neumann, not unknowns): 0 - rhs when
+// WALLRHS (the residual, like the masked rows of SPEC kkt_residual), else 0
+// (the smoother assembles only unknown rows).  Same term order as
+// oracle/stfas.py kkt_residual; 1/h and 1/dt are multiplied, not divided.
+// ---------------------------------------------------------------------------
+template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS>
+__device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const Loc<DIM, PER>& L,
+                                          const bool (&wall)[2 * DIM], int i,
+                                          const R (&VC)[DIM][NbrSlots<DIM>::NB],
+                                          const R (&UC)[DIM][NbrSlots<DIM>::NB], const R (&vp)[2 * DIM],
+                                          const ResP<R>& rhs, bool has_rhs, R (&yu)[2 * DIM + 1],
+                                          R (&yv)[2 * DIM + 1]) {
+  constexpr int NF = 2 * DIM;
+  const auto& ix = cx.ix;
+  const R* Pi = cx.P + (int64_t)i * cx.nc;
+  const R* PBi = cx.PB + (int64_t)i * cx.nc;
+  const R pc = Pi[L.co], pbc = PBi[L.co];
+  const bool inner = cx.inner(i);
+  const Face3<R> Un = inner ? cx.u_next(i) : Face3<R>{};
+  const Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Face3<R>{};
+  static_for<NF>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    constexpr int j = q >> 1, sd = q & 1;
+    if constexpr (!BOTH && sd == 1) {
+      yu[q] = R(0);
+      yv[q] = R(0);
+    } else {
+      const int64_t oo = (int64_t)i * cx.nf[j] + L.of[q];
+      if (wall[q]) {
+        yu[q] = (WALLRHS && has_rhs) ? R(0) - rhs.R3[j][oo] : R(0);
+        yv[q] = (WALLRHS && has_rhs) ? R(0) - rhs.R1[j][oo] : R(0);
+      } else {
+        // the other cell of the face (exists: the face is not a wall)
+        const R pn = L.cell(ix, Pi, j == 0 ? (sd ? 1 : -1) : 0, j == 1 ? (sd ? 1 : -1) : 0,
+                            j == 2 ? (sd ? 1 : -1) : 0);
+        const R pbn = L.cell(ix, PBi, j == 0 ? (sd ? 1 : -1) : 0, j == 1 ? (sd ? 1 : -1) : 0,
+                             j == 2 ? (sd ? 1 : -1) : 0);
+        const R gp = sd ? (pn - pc) * cx.ih : (pc - pn) * cx.ih;
+        const R gpb = sd ? (pbn - pbc) * cx.ih : (pbc - pbn) * cx.ih;
+        const R vf = VC[j][sd + 1], uf = UC[j][sd + 1];
+        const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC, VC, true, true);
+        R a = (((vf - vp[q]) * cx.idt + adv) - uf) + gp;
+        R t1 = R(0);
+        if (inner) t1 = cx.kr * (vf - Vs.c[j][L.of[q]]) - Un.c[j][L.of[q]] * cx.idt;
+        const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC, UC) - S_cached<DIM, j, sd, R>(cx.c0, VC, UC, true, true);
+        R b = ((t1 + uf * cx.idt) + jt) + gpb;
+        if (has_rhs) {
+          a -= rhs.R3[j][oo];
+          b -= rhs.R1[j][oo];
+        }
+        yu[q] = a;
+        yv[q] = b;
+      }
     }
-    out.R1[j][t] = a;
-    out.R3[j][t] = b;
+  });
+  R dv = R(0), du = R(0);
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    R a = (VC[k][2] - VC[k][1]) * cx.ih;
+    R b = (UC[k][2] - UC[k][1]) * cx.ih;
+    dv = (k == 0) ? a : dv + a;
+    du = (k == 0) ? b : du + b;
   }
+  if (has_rhs) {
+    const int64_t o = (int64_t)i * cx.nc + L.co;
+    du -= rhs.R4[o];
+    dv -= rhs.R2[o];
+  }
+  yu[NF] = du;
+  yv[NF] = dv;
 }
 
+// Eq. 8 residual f(x) - rhs, one thread per (frame, cell): the cell's lower
+// faces (R1, R3 of every component), the cell (R2, R4), and under Neumann the
+// upper wall face of the last cell along each axis (0 - rhs).  Neighbour
+// values come from the register caches (every V / U value the cell's faces
+// need is read once per thread, through L1).
 template <int DIM, bool PER, class R>
-__global__ void k_kkt_cells(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
+__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
+  constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
+  const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
   SMK_GRID_STRIDE(t, (int64_t)cx.N * nc) {
-    int i = (int)(t / nc);
+    const int i = (int)(t / nc);
     int c[3];
-    cx.ix.cell_idx(t - (int64_t)i * nc, c);
-    R a = cx.r2(i, c), b = cx.r4(i, c);
-    if (has_rhs) {
-      a -= rhs.R2[t];
-      b -= rhs.R4[t];
+    ix.cell_idx(t - (int64_t)i * nc, c);
+    const Loc<DIM, PER> L(ix, c);
+    bool wall[NF];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      wall[2 * k] = !PER && c[k] == 0;
+      wall[2 * k + 1] = !PER && c[k] == ix.n(k) - 1;
     }
-    out.R2[t] = a;
-    out.R4[t] = b;
+    R VC[DIM][NB], UC[DIM][NB];
+    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
+    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.U, i, cx.nf), UC);
+    const Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
+    R vp[NF];
+#pragma unroll
+    for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
+    R yu[B], yv[B];
+    pair_rows<DIM, PER, R, false, true>(cx, L, wall, i, VC, UC, vp, rhs, has_rhs != 0, yu, yv);
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      const int64_t o = (int64_t)i * cx.nf[k] + L.of[2 * k];
+      out.R3[k][o] = yu[2 * k];
+      out.R1[k][o] = yv[2 * k];
+      if (!PER && wall[2 * k + 1]) {
+        const int64_t ou = (int64_t)i * cx.nf[k] + L.of[2 * k + 1];
+        out.R3[k][ou] = has_rhs ? R(0) - rhs.R3[k][ou] : R(0);
+        out.R1[k][ou] = has_rhs ? R(0) - rhs.R1[k][ou] : R(0);
+      }
+    }
+    const int64_t oc = (int64_t)i * nc + L.co;
+    out.R4[oc] = yu[NF];
+    out.R2[oc] = yv[NF];
   }
 }
 
@@ -163,6 +205,7 @@ __global__ void k_kkt_cells(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, Re
 template <class R, int B, int C, bool PIVOT>
 __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) {
   bool ok = true;
+  R inv[B];
 #pragma unroll
   for (int col = 0; col < B; ++col) {
     if (PIVOT) {
@@ -185,10 +228,10 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
     }
     R piv = A[col][col];
     if (!(rabs(piv) > tiny)) ok = false;
-    R inv = R(1) / piv;
+    inv[col] = R(1) / piv;
 #pragma unroll
     for (int r = col + 1; r < B; ++r) {
-      R fct = A[r][col] * inv;
+      R fct = A[r][col] * inv[col];
 #pragma unroll
       for (int c = col + 1; c < B; ++c) A[r][c] -= fct * A[col][c];
 #pragma unroll
@@ -197,15 +240,54 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
   }
 #pragma unroll
   for (int r = B - 1; r >= 0; --r) {
-    R inv = R(1) / A[r][r];
 #pragma unroll
     for (int c = 0; c < C; ++c) {
       R s = X[r][c];
 #pragma unroll
       for (int q = r + 1; q < B; ++q) s -= A[r][q] * X[q][c];
-      X[r][c] = s * inv;
+      X[r][c] = s * inv[r];
     }
   }
+  return ok;
+}
+
+// The partially pivoted solve runs once per cell line (the last global pair,
+// alpha = 0, whose faces block is singular along M^-1 g); it is kept out of
+// line on a local-memory copy so its unrolled row swaps do not bloat the
+// consumer loop or pin A / X to local memory.
+template <class R, int B, int C>
+__device__ __noinline__ bool dense_solve_pivot_mem(R* T, R tiny) {
+  R A[B][B], X[B][C];
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+#pragma unroll
+    for (int c = 0; c < B; ++c) A[r][c] = T[r * (B + C) + c];
+#pragma unroll
+    for (int c = 0; c < C; ++c) X[r][c] = T[r * (B + C) + B + c];
+  }
+  bool ok = dense_solve<R, B, C, true>(A, X, tiny);
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) T[r * (B + C) + B + c] = X[r][c];
+  return ok;
+}
+
+template <class R, int B, int C>
+__device__ __forceinline__ bool dense_solve_pivot(R (&A)[B][B], R (&X)[B][C], R tiny) {
+  R T[B * (B + C)];
+#pragma unroll
+  for (int r = 0; r < B; ++r) {
+#pragma unroll
+    for (int c = 0; c < B; ++c) T[r * (B + C) + c] = A[r][c];
+#pragma unroll
+    for (int c = 0; c < C; ++c) T[r * (B + C) + B + c] = X[r][c];
+  }
+  bool ok = dense_solve_pivot_mem<R, B, C>(T, tiny);
+#pragma unroll
+  for (int r = 0; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) X[r][c] = T[r * (B + C) + B + c];
   return ok;
 }
 
@@ -256,23 +338,15 @@ struct CellGeo {
 //                             (k,0) = -c0/2 v_j[c + s e_j - e_k]
 // Wall rows / columns are zero (not unknowns).  Equal to the probed Jacobian
 // of oracle/stfas.local_jacobian up to rounding.
-template <int DIM, bool PER, class R>
-__device__ __forceinline__ void local_jacobian(const Ix<DIM, PER>& ix, R c0, const Face3<R>& v,
-                                               const CellGeo<DIM, PER, R>& cg, R (&J)[2 * DIM][2 * DIM]) {
+template <int DIM, class R>
+__device__ __forceinline__ void jac_cached(R c0, R idt, const R (&v)[DIM][NbrSlots<DIM>::NB],
+                                           const bool (&wall)[2 * DIM], R (&J)[2 * DIM][2 * DIM]) {
   constexpr int NF = 2 * DIM;
-  const int* c = cg.c;
   const R hc = R(0.5) * c0;
 #pragma unroll
   for (int j = 0; j < DIM; ++j) {
-    int t[3];
-    shift((int*)c, j, -1, t);
-    R vm = ix.face(v.c[j], j, t[0], t[1], t[2]);
-    R v0 = ix.face(v.c[j], j, c[0], c[1], c[2]);
-    shift((int*)c, j, 1, t);
-    R v1 = ix.face(v.c[j], j, t[0], t[1], t[2]);
-    shift((int*)c, j, 2, t);
-    R v2 = ix.face(v.c[j], j, t[0], t[1], t[2]);
-    R vc = R(0.5) * (v0 + v1);
+    const R vm = v[j][0], v0 = v[j][1], v1 = v[j][2], v2 = v[j][3];
+    const R vc = R(0.5) * (v0 + v1);
     J[2 * j][2 * j] = hc * (v1 - vm);
     J[2 * j][2 * j + 1] = c0 * vc + hc * v1;
     J[2 * j + 1][2 * j] = -c0 * vc - hc * v0;
@@ -282,12 +356,8 @@ __device__ __forceinline__ void local_jacobian(const Ix<DIM, PER>& ix, R c0, con
       if (k == j) continue;
 #pragma unroll
       for (int sr = 0; sr < 2; ++sr) {
-        int f[3], q[3];
-        shift((int*)c, j, sr, f);
-        shift(f, k, 1, q);
-        J[2 * j + sr][2 * k + 1] = hc * ix.face(v.c[j], j, q[0], q[1], q[2]);
-        shift(f, k, -1, q);
-        J[2 * j + sr][2 * k] = -hc * ix.face(v.c[j], j, q[0], q[1], q[2]);
+        J[2 * j + sr][2 * k + 1] = hc * v[j][nbr_slot<DIM>(j, sr, k, 1)];
+        J[2 * j + sr][2 * k] = -hc * v[j][nbr_slot<DIM>(j, sr, k, -1)];
       }
     }
   }
@@ -295,94 +365,18 @@ __device__ __forceinline__ void local_jacobian(const Ix<DIM, PER>& ix, R c0, con
   for (int a = 0; a < NF; ++a)
 #pragma unroll
     for (int b = 0; b < NF; ++b)
-      if (cg.wall[a] || cg.wall[b]) J[a][b] = R(0);
-}
-
-// assembled per (cell, frame) entries: yU[B], yV[B]
-template <int DIM>
-struct AsmLayout {
-  static constexpr int NF = 2 * DIM, B = NF + 1;
-  static constexpr int E = 2 * B;
-};
-
-// Phase 1 (parallel over colour cells x frames): local residual rows
-// -(f - rhs) of both blocks of pair i.  Layout asm[(i * E + e) * M + m]
-// (coalesced in m).
-template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0,
-                                                       int o1, int o2, int mod, int m0, int m1, int m2,
-                                                       R* __restrict__ asmb) {
-  constexpr int NF = AsmLayout<DIM>::NF, B = AsmLayout<DIM>::B, E = AsmLayout<DIM>::E;
-  const int64_t M = (int64_t)m0 * m1 * m2;
-  const auto& ix = cx.ix;
-  SMK_GRID_STRIDE(t, (int64_t)cx.N * M) {
-    const int i = (int)(t / M);
-    const int64_t m = t - (int64_t)i * M;
-    CellGeo<DIM, PER, R> cg(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
-    R* out = asmb + (int64_t)i * E * M + m;
-    const int* c = cg.c;
-    Face3<R> Vi = frame_of(cx.V, i, cx.nf);
-    Face3<R> Ui = frame_of(cx.U, i, cx.nf);
-    Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
-    const bool inner = cx.inner(i);
-    Face3<R> Un = inner ? cx.u_next(i) : Vi;
-    Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Vi;
-    NbrField<DIM, PER, R> VC(ix, c, Vi), UC(ix, c, Ui);
-    const R* Pi = cx.P + (int64_t)i * cx.nc;
-    const R* PBi = cx.PB + (int64_t)i * cx.nc;
-    const R pc = ix.cell(Pi, c[0], c[1], c[2]), pbc = ix.cell(PBi, c[0], c[1], c[2]);
-    static_for<NF>([&](auto qc) {
-      constexpr int q = decltype(qc)::value;
-      constexpr int j = q >> 1, sd = q & 1;
-      R yu = R(0), yv = R(0);
-      if (!cg.wall[q]) {
-        int nb[3] = {c[0], c[1], c[2]};
-        nb[j] += sd ? 1 : -1;                         // the other cell of the face
-        const R pn = ix.cell(Pi, nb[0], nb[1], nb[2]), pbn = ix.cell(PBi, nb[0], nb[1], nb[2]);
-        const R gp = sd ? (pn - pc) / cx.h : (pc - pn) / cx.h;
-        const R gpb = sd ? (pbn - pbc) / cx.h : (pbc - pbn) / cx.h;
-        const R vf = VC.val[j][sd + 1], uf = UC.val[j][sd + 1];
-        const int64_t o = ix.face_off(j, cg.fidx[q][0], cg.fidx[q][1], cg.fidx[q][2]);
-        // cells above / below the face exist for every non-wall face
-        const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC.val, VC.val, true, true);
-        yu = (((vf - Vp.c[j][o]) / cx.dt + adv) - uf) + gp;
-        R t1 = R(0);
-        if (inner) t1 = cx.kr * (vf - Vs.c[j][o]) - Un.c[j][o] / cx.dt;
-        const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC.val, UC.val) -
-                     S_cached<DIM, j, sd, R>(cx.c0, VC.val, UC.val, true, true);
-        yv = ((t1 + uf / cx.dt) + jt) + gpb;
-        if (has_rhs) {
-          const int64_t oo = (int64_t)i * cx.nf[j] + o;
-          yu -= rhs.R3[j][oo];
-          yv -= rhs.R1[j][oo];
-        }
-      }
-      out[(int64_t)q * M] = -yu;
-      out[(int64_t)(B + q) * M] = -yv;
-    });
-    {
-      R dv = R(0), du = R(0);
+      if (wall[a] || wall[b]) J[a][b] = R(0);
+  // M = I/dt + J on the unknown faces
 #pragma unroll
-      for (int k = 0; k < DIM; ++k) {
-        R a = (VC.val[k][2] - VC.val[k][1]) / cx.h;
-        R b = (UC.val[k][2] - UC.val[k][1]) / cx.h;
-        dv = (k == 0) ? a : dv + a;
-        du = (k == 0) ? b : du + b;
-      }
-      R yu = du, yv = dv;
-      if (has_rhs) {
-        int64_t o = (int64_t)i * cx.nc + ix.cell_off(c[0], c[1], c[2]);
-        yu -= rhs.R4[o];
-        yv -= rhs.R2[o];
-      }
-      out[(int64_t)NF * M] = -yu;
-      out[(int64_t)(B + NF) * M] = -yv;
-    }
-  }
+  for (int q = 0; q < NF; ++q)
+    if (!wall[q]) J[q][q] += idt;
 }
 
-// Phase 2 (one thread per colour cell): the cell's 2N-block Eq. 9 time line,
-// solved exactly with the u-blocks eliminated in closed form.
+// ---------------------------------------------------------------------------
+// One colour pass = k_scgs_fwd (forward elimination) + k_scgs_back (back
+// substitution) + k_scgs_apply.  Every cell of the colour solves its 2N-block
+// Eq. 9 time line exactly (oracle/stfas.py scgs_color), the
+// state is read-only until k_scgs_apply (snapshot semantics).
 //
 // The u-block of pair i is the constant saddle [[-I, g], [-g^T, 0]] (g = the
 // cell's grad column), coupled to v_i by -I/dt and to v_{i+1} by
@@ -390,242 +384,298 @@ __global__ void __launch_bounds__(256) k_scgs_assemble(KktCtx<DIM, PER, R> cx, R
 //     du_i = -c_i - (P/dt) dv_i + P M_i dv_{i+1},   c_i = P yu_i + g yp_i / sigma,
 //     dp_{i+1} = (g^T a_i - yp_i) / sigma,   a_i = yu_i + dv_i/dt - M_i dv_{i+1}.
 // Substituting into the v-rows leaves a symmetric block-tridiagonal system in
-// (dv_{i+1}, dpbar_{i+1}) only (N blocks instead of 2N):
-//     D_i  = M_i^T P M_i + alpha_i I + [i+1<N] P/dt^2     (faces; + the g saddle)
-//     L_i  = -M_i^T P / dt     (to dv_i),   U_i = L_{i+1}^T = -P M_{i+1} / dt
+// (dv_{i+1}, dpbar_{i+1}) only (N blocks of 2d+1 instead of 2N):
+//     D_i  = (P M_i)^T (P M_i) + alpha_i I + [i+1<N] P/dt^2   (faces; + the g saddle)
+//     L_i  = -(P M_i)^T / dt   (to dv_i),   U_i = L_{i+1}^T = -P M_{i+1} / dt
 //     rhs  = yv_i + M_i^T c_i - [i+1<N] c_{i+1} / dt.
-// This is exact block elimination of the oracle's system (oracle/stfas.py
-// block_thomas), so iterates agree to rounding.  Fill-in per pair: W (B x NF)
-// and z (B), layout [pair][entry][m].
+//
+// k_scgs_fwd is warp-specialised.  A CTA owns TM colour cells; warps
+// [0, TM/32) are producers, [TM/32, 2TM/32) consumers, one thread of each per
+// cell.  Producers stream the state (all the HBM reads of the pass): the
+// -(f - rhs) rows of pair i from register caches of the cell's
+// neighbourhood, M_i, and hand P M_i, c_i, yv_i + M_i^T c_i and the dpbar row
+// to the consumers through an S-stage shared-memory ring (named barriers
+// FULL/EMPTY per stage); they also store the u-rows yu_i for the backward
+// pass.  Consumers run the dense elimination: per pair one (2d+1)-block solve
+// with 2d+1 right-hand sides, carrying the Schur-updated D_{i+1}, its partial
+// rhs and (P M_{i+1})^T z_i to the next pair, and store W_i (B x NF) and z_i
+// (B).  Per pair the scratch holds SE values, layout [pair][entry][m].
+// ---------------------------------------------------------------------------
+template <int DIM>
+struct Line {
+  static constexpr int NF = 2 * DIM, B = NF + 1;
+  static constexpr int SE = B * (NF + 2);                // W, z, yu
+  static constexpr int W0 = 0, Z0 = B * NF, Y0 = B * NF + B;
+  static constexpr int NE = NF * NF + 2 * NF + 1;        // ring entry: PM, c, xr, ycell
+  static constexpr int E_PM = 0, E_C = NF * NF, E_XR = NF * NF + NF, E_YC = NF * NF + 2 * NF;
+  static constexpr int S = 3;                            // ring stages
+};
+
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// per-cell constants shared by the smoother kernels
 template <int DIM, bool PER, class R>
-__device__ __forceinline__ void load_rows(const R* __restrict__ in, int64_t M, R (&yu)[2 * DIM + 1],
-                                          R (&yv)[2 * DIM + 1]) {
-  constexpr int B = 2 * DIM + 1;
+struct LineCell {
+  static constexpr int NF = 2 * DIM;
+  CellGeo<DIM, PER, R> cg;
+  R isig;
+  __device__ __forceinline__ LineCell(const Ix<DIM, PER>& ix, R h, int64_t m, int o0, int o1, int o2, int mod, int m1,
+                                      int m2)
+      : cg(ix, h, m, o0, o1, o2, mod, m1, m2) {
+    R sigma = R(0);
 #pragma unroll
-  for (int q = 0; q < B; ++q) {
-    yu[q] = __ldg(in + (int64_t)q * M);
-    yv[q] = __ldg(in + (int64_t)(B + q) * M);
+    for (int q = 0; q < NF; ++q) sigma += cg.gcol[q] * cg.gcol[q];
+    isig = R(1) / sigma;
   }
-}
-
-template <int DIM, bool PER, class R>
-__device__ __forceinline__ void frame_M(const Ix<DIM, PER>& ix, R c0, const Face3<R>& V, int i,
-                                        const CellGeo<DIM, PER, R>& cg, R idt, R (&Mx)[2 * DIM][2 * DIM]) {
-  Face3<R> Vi;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) Vi.c[k] = k < DIM ? V.c[k] + (int64_t)i * ix.faces(k) : nullptr;
-  local_jacobian<DIM, PER, R>(ix, c0, Vi, cg, Mx);
-#pragma unroll
-  for (int q = 0; q < 2 * DIM; ++q)
-    if (!cg.wall[q]) Mx[q][q] += idt;
-}
-
-template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R kr, int N, int t0, int Ng, Face3<R> V,
-                                                  int o0, int o1, int o2, int mod, int m0, int m1, int m2, R omega,
-                                                  const R* __restrict__ asmb, R* __restrict__ scratch,
-                                                  R* __restrict__ xout, int* flag) {
-  constexpr int NF = Slots<DIM>::NF, B = Slots<DIM>::B, C = Slots<DIM>::C, E = AsmLayout<DIM>::E;
-  const int64_t M = (int64_t)m0 * m1 * m2;
-  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
-  CellGeo<DIM, PER, R> cg(ix, h, m, o0, o1, o2, mod, m1, m2);
-  const R c0 = R(0.5) / h;
-  const R idt = R(1) / dt;
-  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
-  R sigma = R(0);
-#pragma unroll
-  for (int q = 0; q < NF; ++q) sigma += cg.gcol[q] * cg.gcol[q];
-  const R isig = R(1) / sigma;
-  // P x = x - g (g^T x) / sigma on non-wall slots (g is zero on walls)
-  auto projP = [&](R (&x)[NF]) {
+  // P x on the unknown faces (g is zero on walls)
+  __device__ __forceinline__ void projP(R (&x)[NF]) const {
     R d = R(0);
 #pragma unroll
     for (int q = 0; q < NF; ++q) d += cg.gcol[q] * x[q];
     d *= isig;
 #pragma unroll
     for (int q = 0; q < NF; ++q) x[q] = cg.wall[q] ? R(0) : x[q] - cg.gcol[q] * d;
-  };
-  bool ok = true;
-  R zprev[B];
-  R Wprev[B][NF];
-#pragma unroll
-  for (int a = 0; a < B; ++a) {
-    zprev[a] = R(0);
-#pragma unroll
-    for (int b = 0; b < NF; ++b) Wprev[a][b] = R(0);
   }
-  R Mc[NF][NF];   // M_i for the current pair
-  frame_M<DIM, PER, R>(ix, c0, V, 0, cg, idt, Mc);
-  R cc[NF];       // c_i
-  {
-    R yu[B], yv[B];
-    load_rows<DIM, PER, R>(asmb + m, M, yu, yv);
+};
+
+template <int DIM, bool PER, class R, int TM>
+__global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1,
+                                                     int o2, int mod, int m0, int m1, int m2, R* __restrict__ scratch,
+                                                     int* flag) {
+  using LN = Line<DIM>;
+  constexpr int NF = LN::NF, B = LN::B, C = NF + 1, NB = NbrSlots<DIM>::NB, NE = LN::NE, S = LN::S;
+  constexpr int NT = 2 * TM;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* ring = reinterpret_cast<R*>(smem_raw);   // [S][NE][TM]
+  const auto& ix = cx.ix;
+  const int N = cx.N;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const bool producer = threadIdx.x < TM;
+  const int lane = producer ? threadIdx.x : threadIdx.x - TM;
+  const int64_t m = (int64_t)blockIdx.x * TM + lane;
+  const bool act = m < M;   // inactive threads still take part in every barrier
+  const LineCell<DIM, PER, R> lc(ix, cx.h, act ? m : 0, o0, o1, o2, mod, m1, m2);
+  const auto& cg = lc.cg;
+  const R c0 = cx.c0;
+  const R idt = cx.idt;
+  auto sc = [&](int i, int e) -> R* { return scratch + ((int64_t)i * LN::SE + e) * M + m; };
+  auto slot = [&](int i, int e) -> R* { return ring + ((i % S) * NE + e) * TM + lane; };
+
+  if (producer) {
+    const Loc<DIM, PER> L(ix, cg.c);
+    const bool hr = has_rhs != 0;
+    R vp[NF];   // V_{i-1} at the own faces
 #pragma unroll
-    for (int q = 0; q < NF; ++q) cc[q] = yu[q];
-    projP(cc);
+    for (int q = 0; q < NF; ++q) vp[q] = act ? cx.v0.c[q >> 1][L.of[q]] : R(0);
+    for (int i = 0; i < N; ++i) {
+      if (i >= S) nb_sync(1 + S + i % S, NT);   // EMPTY: the consumers released pair i - S
+      if (act) {
+        R VC[DIM][NB], UC[DIM][NB];
+        R yu[B], yv[B];
+        load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
+        load_nbr<DIM, PER, R>(ix, L, frame_of(cx.U, i, cx.nf), UC);
+        pair_rows<DIM, PER, R, true, false>(cx, L, cg.wall, i, VC, UC, vp, rhs, hr, yu, yv);
 #pragma unroll
-    for (int q = 0; q < NF; ++q) cc[q] += cg.gcol[q] * yu[NF] * isig;
+        for (int q = 0; q < B; ++q) {
+          yu[q] = -yu[q];
+          yv[q] = -yv[q];
+          *sc(i, LN::Y0 + q) = yu[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NF; ++q) vp[q] = VC[q >> 1][(q & 1) + 1];
+        R Mx[NF][NF], cv[NF];
+        jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
+#pragma unroll
+        for (int q = 0; q < NF; ++q) cv[q] = yu[q];
+        lc.projP(cv);
+#pragma unroll
+        for (int q = 0; q < NF; ++q) cv[q] += cg.gcol[q] * yu[NF] * lc.isig;
+#pragma unroll
+        for (int a = 0; a < NF; ++a) {
+          R s = yv[a];
+#pragma unroll
+          for (int t = 0; t < NF; ++t) s += Mx[t][a] * cv[t];
+          *slot(i, LN::E_XR + a) = s;
+          *slot(i, LN::E_C + a) = cv[a];
+        }
+        *slot(i, LN::E_YC) = yv[NF];
+#pragma unroll
+        for (int b = 0; b < NF; ++b) {
+          R col[NF];
+#pragma unroll
+          for (int a = 0; a < NF; ++a) col[a] = Mx[a][b];
+          lc.projP(col);
+#pragma unroll
+          for (int a = 0; a < NF; ++a) *slot(i, LN::E_PM + a * NF + b) = col[a];
+        }
+      }
+      nb_arrive(1 + i % S, NT);   // FULL
+    }
+    return;
   }
 
-  for (int i = 0; i < N; ++i) {
-    const bool has_next = i + 1 < N;
-    R yu[B], yv[B];
-    load_rows<DIM, PER, R>(asmb + (int64_t)i * E * M + m, M, yu, yv);
-    // PM = P M_i (column-wise projection)
-    R PM[NF][NF];
-#pragma unroll
-    for (int b = 0; b < NF; ++b) {
-      R col[NF];
-#pragma unroll
-      for (int a = 0; a < NF; ++a) col[a] = Mc[a][b];
-      projP(col);
-#pragma unroll
-      for (int a = 0; a < NF; ++a) PM[a][b] = col[a];
-    }
-    R A[B][B], X[B][C];
-    const R alpha = (t0 + i < Ng - 1) ? kr : R(0);
-    // D_i faces: M^T P M + alpha I + [has_next] P/dt^2
+  // ---------------- consumers ----------------
+  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+  auto load_pm = [&](int i, R (&PM)[NF][NF]) {
 #pragma unroll
     for (int a = 0; a < NF; ++a)
 #pragma unroll
-      for (int b = 0; b < NF; ++b) {
+      for (int b = 0; b < NF; ++b) PM[a][b] = *slot(i, LN::E_PM + a * NF + b);
+  };
+  // D faces block of pair ip: (PM)^T PM + [ip+1<N] P/dt^2 + alpha / wall identity
+  auto diag_block = [&](int ip, const R (&PM)[NF][NF], R (&Af)[NF][NF]) {
+    const bool nx = ip + 1 < N;
+    const R alpha = (cx.t0 + ip < cx.Ng - 1) ? cx.kr : R(0);
+#pragma unroll
+    for (int a = 0; a < NF; ++a)
+#pragma unroll
+      for (int b = a; b < NF; ++b) {
         R s = R(0);
 #pragma unroll
-        for (int t = 0; t < NF; ++t) s += Mc[t][a] * PM[t][b];
-        if (has_next) {
-          R pab = (a == b && !cg.wall[a] ? R(1) : R(0)) - cg.gcol[a] * cg.gcol[b] * isig;
+        for (int t = 0; t < NF; ++t) s += PM[t][a] * PM[t][b];
+        if (nx) {
+          R pab = (a == b && !cg.wall[a] ? R(1) : R(0)) - cg.gcol[a] * cg.gcol[b] * lc.isig;
           s += pab * idt * idt;
         }
-        A[a][b] = s;
+        Af[a][b] = s;
+        Af[b][a] = s;
       }
 #pragma unroll
-    for (int q = 0; q < NF; ++q) {
-      A[q][q] += cg.wall[q] ? R(1) : alpha;
-      A[q][NF] = cg.gcol[q];
-      A[NF][q] = -cg.gcol[q];
-    }
-    A[NF][NF] = R(0);
-    // reduced rhs: yv + M^T c_i - [has_next] c_{i+1}/dt
-    R cn[NF];
-    if (has_next) {
-      R yun[B], yvn[B];
-      load_rows<DIM, PER, R>(asmb + (int64_t)(i + 1) * E * M + m, M, yun, yvn);
-#pragma unroll
-      for (int q = 0; q < NF; ++q) cn[q] = yun[q];
-      projP(cn);
-#pragma unroll
-      for (int q = 0; q < NF; ++q) cn[q] += cg.gcol[q] * yun[NF] * isig;
-    } else {
-#pragma unroll
-      for (int q = 0; q < NF; ++q) cn[q] = R(0);
-    }
+    for (int q = 0; q < NF; ++q) Af[q][q] += cg.wall[q] ? R(1) : alpha;
+  };
+  R Af[NF][NF];   // Schur-updated faces block of the current pair
+  R xr[NF];       // its partial rhs yv + M^T c
+  R sz[NF];       // (P M)^T z_{i-1}
+  R ycell;        // its dpbar-row rhs
+  bool ok = true;
+  nb_sync(1 + 0, NT);
+  {
+    R PM[NF][NF];
+    load_pm(0, PM);
+    diag_block(0, PM, Af);
 #pragma unroll
     for (int a = 0; a < NF; ++a) {
-      R s = yv[a];
-#pragma unroll
-      for (int t = 0; t < NF; ++t) s += Mc[t][a] * cc[t];
-      X[a][NF] = cg.wall[a] ? R(0) : s - cn[a] * idt;
+      xr[a] = *slot(0, LN::E_XR + a);
+      sz[a] = R(0);
     }
-    X[NF][NF] = yv[NF];
-    // lower coupling L_i = -(P M_i)^T / dt to dv_i:  A -= L Wprev, rhs -= L zprev
-    if (i > 0) {
+    ycell = *slot(0, LN::E_YC);
+  }
+  for (int i = 0; i < N; ++i) {
+    const bool has_next = i + 1 < N;
+    if (has_next) nb_sync(1 + (i + 1) % S, NT);   // FULL: pair i+1 ready
+    R A[B][B], X[B][C];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) {
+#pragma unroll
+      for (int b = 0; b < NF; ++b) A[a][b] = Af[a][b];
+      A[a][NF] = cg.gcol[a];
+      A[NF][a] = -cg.gcol[a];
+      const R cn = has_next ? *slot(i + 1, LN::E_C + a) : R(0);
+      R s = cg.wall[a] ? R(0) : xr[a] - cn * idt;
+      if (i > 0) s += sz[a] * idt;
+      X[a][NF] = s;
+#pragma unroll
+      for (int b = 0; b < NF; ++b) X[a][b] = has_next ? -*slot(i + 1, LN::E_PM + a * NF + b) * idt : R(0);
+      X[NF][a] = R(0);
+    }
+    A[NF][NF] = R(0);
+    X[NF][NF] = ycell;
+    if (cx.t0 + i < cx.Ng - 1) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
+    else ok &= dense_solve_pivot<R, B, C>(A, X, tinyv);
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q) *sc(i, LN::W0 + r * NF + q) = X[r][q];
+        *sc(i, LN::Z0 + r) = X[r][NF];
+      }
+    }
+    nb_arrive(1 + S + i % S, NT);   // EMPTY: pair i released
+    if (has_next) {
+      R PM[NF][NF];
+      load_pm(i + 1, PM);
+      diag_block(i + 1, PM, Af);
+      // Schur complement of the eliminated pair: + (P M)^T W_i / dt (symmetric)
 #pragma unroll
       for (int a = 0; a < NF; ++a) {
 #pragma unroll
-        for (int b = 0; b < NF; ++b) {
+        for (int b = a; b < NF; ++b) {
           R s = R(0);
 #pragma unroll
-          for (int t = 0; t < NF; ++t) s += PM[t][a] * Wprev[t][b];
-          A[a][b] += s * idt;
+          for (int t = 0; t < NF; ++t) s += PM[t][a] * X[t][b];
+          Af[a][b] += s * idt;
+          if (b != a) Af[b][a] += s * idt;
         }
         R s = R(0);
 #pragma unroll
-        for (int t = 0; t < NF; ++t) s += PM[t][a] * zprev[t];
-        X[a][NF] += s * idt;
+        for (int t = 0; t < NF; ++t) s += PM[t][a] * X[t][NF];
+        sz[a] = s;
+        xr[a] = *slot(i + 1, LN::E_XR + a);
       }
-    }
-    // upper coupling U_i = -P M_{i+1} / dt (columns), load M_{i+1} first
-    R Mn[NF][NF];
-    if (has_next) {
-      frame_M<DIM, PER, R>(ix, c0, V, i + 1, cg, idt, Mn);
-#pragma unroll
-      for (int b = 0; b < NF; ++b) {
-        R col[NF];
-#pragma unroll
-        for (int a = 0; a < NF; ++a) col[a] = Mn[a][b];
-        projP(col);
-#pragma unroll
-        for (int a = 0; a < B; ++a) X[a][b] = a < NF ? -col[a] * idt : R(0);
-      }
-    } else {
-#pragma unroll
-      for (int a = 0; a < B; ++a)
-#pragma unroll
-        for (int b = 0; b < NF; ++b) X[a][b] = R(0);
-    }
-    if (alpha > R(0)) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
-    else ok &= dense_solve<R, B, C, true>(A, X, tinyv);
-    R* base = scratch + (int64_t)i * B * C * M + m;
-#pragma unroll
-    for (int r = 0; r < B; ++r) {
-#pragma unroll
-      for (int q = 0; q < C; ++q) base[(int64_t)(r * C + q) * M] = X[r][q];
-      zprev[r] = X[r][NF];
-#pragma unroll
-      for (int q = 0; q < NF; ++q) Wprev[r][q] = X[r][q];
-    }
-    if (has_next) {
-#pragma unroll
-      for (int a = 0; a < NF; ++a) {
-        cc[a] = cn[a];
-#pragma unroll
-        for (int b = 0; b < NF; ++b) Mc[a][b] = Mn[a][b];
-      }
+      ycell = *slot(i + 1, LN::E_YC);
     }
   }
+  if (act && !ok) atomicExch(flag, 1);
+}
 
-  // ---- backward: dv (and dpbar) per pair, then du / dp of pair i+1 ----
-  // u-block of pair i needs dv_i (pair i-1) and dv_{i+1} (pair i)
+// Back substitution of one colour: dv, dpbar of pair i from the stored W_i,
+// z_i, then du, dp of pair i+1 (needs dv_{i+1}, dv_{i+2}, yu_{i+1} and
+// M_{i+1}, recomputed from V).  Writes omega * deltas to xout
+// [2 * pair + (0: u-block, 1: v-block)][entry][m].
+template <int DIM, bool PER, class R>
+__global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
+                                                   int m1, int m2, R omega, const R* __restrict__ scratch,
+                                                   R* __restrict__ xout) {
+  using LN = Line<DIM>;
+  constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB;
+  const auto& ix = cx.ix;
+  const int N = cx.N;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= M) return;
+  const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
+  const auto& cg = lc.cg;
+  const Loc<DIM, PER> L(ix, cg.c);
+  const R idt = cx.idt;
+  auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
   auto u_delta = [&](int i, const R (&dvi)[NF], const R (&dvn)[NF]) {
-    R Mi[NF][NF];
-    frame_M<DIM, PER, R>(ix, c0, V, i, cg, idt, Mi);
-    R yu[B], yv[B];
-    load_rows<DIM, PER, R>(asmb + (int64_t)i * E * M + m, M, yu, yv);
+    R VC[DIM][NB], Mi[NF][NF];
+    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
+    jac_cached<DIM, R>(cx.c0, idt, VC, cg.wall, Mi);
     R a[NF];
     R ga = R(0);
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
-      R s = yu[q] + dvi[q] * idt;
+      R s = sc(i, LN::Y0 + q) + dvi[q] * idt;
 #pragma unroll
       for (int t = 0; t < NF; ++t) s -= Mi[q][t] * dvn[t];
       a[q] = cg.wall[q] ? R(0) : s;
       ga += cg.gcol[q] * a[q];
     }
-    R dp = (ga - yu[NF]) * isig;
+    const R dp = (ga - sc(i, LN::Y0 + NF)) * lc.isig;
     R* xo = xout + (int64_t)(2 * i) * B * M + m;
 #pragma unroll
     for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
     xo[(int64_t)NF * M] = omega * dp;
   };
-  R xn[NF];      // dv of pair i+1 (faces)
-  R xnn[NF];     // dv of pair i+2
+  R xn[NF];   // dv of pair i+1
 #pragma unroll
-  for (int q = 0; q < NF; ++q) xn[q] = xnn[q] = R(0);
+  for (int q = 0; q < NF; ++q) xn[q] = R(0);
   for (int i = N - 1; i >= 0; --i) {
-    const R* base = scratch + (int64_t)i * B * C * M + m;
     R xb[B];
 #pragma unroll
     for (int r = 0; r < B; ++r) {
-      R s = base[(int64_t)(r * C + NF) * M];
+      R s = sc(i, LN::Z0 + r);
 #pragma unroll
-      for (int q = 0; q < NF; ++q) s -= base[(int64_t)(r * C + q) * M] * xn[q];
+      for (int q = 0; q < NF; ++q) s -= sc(i, LN::W0 + r * NF + q) * xn[q];
       xb[r] = s;
     }
     R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
     for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
-    // u-block of pair i+1: dv_{i+1} = xb (this pair), dv_{i+2} = xn
     if (i + 1 < N) {
       R dvi[NF];
 #pragma unroll
@@ -635,14 +685,12 @@ __global__ void __launch_bounds__(128) k_scgs_line(Ix<DIM, PER> ix, R h, R dt, R
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];
   }
-  {
-    R zero[NF];
+  R zero[NF];
 #pragma unroll
-    for (int q = 0; q < NF; ++q) zero[q] = R(0);
-    u_delta(0, zero, xn);   // dv_0 = 0 (pinned / frozen halo)
-  }
-  if (!ok) atomicExch(flag, 1);
+  for (int q = 0; q < NF; ++q) zero[q] = R(0);
+  u_delta(0, zero, xn);   // dv_0 = 0 (pinned / frozen halo)
 }
+
 
 // x += omega * dx on the colour's unknowns (disjoint across cells)
 template <int DIM, bool PER, class R>
@@ -723,8 +771,7 @@ struct Nso : NsoBase {
   std::vector<Level<R>> lv;
   Scratch mem;
   int64_t nbytes = 0;
-  R* scratch = nullptr;   // smoother W/z
-  R* asmb = nullptr;      // smoother assembled entries
+  R* scratch = nullptr;   // smoother fill-in W/z and u-rows (Line<DIM>::SE per pair)
   R* xout = nullptr;      // smoother deltas
   int* flag = nullptr;
   double* parts = nullptr;
@@ -735,10 +782,10 @@ struct Nso : NsoBase {
   bool guide_set = false;
   // optional CUDA-event profile of the smoother's colour kernel
   bool prof = false;
-  static constexpr int NKIND = 3;  // 0 assemble, 1 line solve, 2 apply
+  static constexpr int NKIND = 4;  // 0 forward, 1 apply, 2 residual, 3 backward
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[NKIND];
-  size_t ev_used[NKIND] = {0, 0, 0};
-  int64_t prof_cells[NKIND] = {0, 0, 0};  // cell-timesteps processed
+  size_t ev_used[NKIND] = {0, 0, 0, 0};
+  int64_t prof_cells[NKIND] = {0, 0, 0, 0};  // cell-timesteps processed
 
   void prof_begin(int kind, int64_t M, cudaStream_t st) {
     if (!prof) return;
@@ -800,10 +847,9 @@ struct Nso : NsoBase {
       for (int a = 0; a < DIM; ++a) M *= (L.g.n[a] + p.color_mod - 1) / p.color_mod;
       maxM = M > maxM ? M : maxM;
     }
-    constexpr int B = Slots<DIM>::B, C = Slots<DIM>::C;
-    scratch = alloc((int64_t)N * B * C * maxM);
+    constexpr int B = Slots<DIM>::B;
+    scratch = alloc((int64_t)N * Line<DIM>::SE * maxM);
     xout = alloc((int64_t)2 * N * B * maxM);
-    asmb = alloc((int64_t)N * AsmLayout<DIM>::E * maxM);
     flag = (int*)mem.get(64);
     parts = (double*)mem.get(sizeof(double) * 70000);
     scal = mem.get(64);
@@ -858,6 +904,8 @@ struct Nso : NsoBase {
     c.c0 = (R)(0.5 / L.g.h);
     c.h = (R)L.g.h;
     c.dt = (R)prm.dt;
+    c.ih = (R)(1.0 / L.g.h);
+    c.idt = (R)(1.0 / prm.dt);
     c.kr = (R)(prm.K / prm.r);
     c.N = prm.n_frames;
     for (int k = 0; k < 3; ++k) c.nf[k] = L.nf[k];
@@ -886,12 +934,11 @@ struct Nso : NsoBase {
 
   void residual(int l, const StP<R>& s, const ResP<R>* rhs, const ResP<R>& out, cudaStream_t st) {
     auto c = ctx(l, s);
-    int64_t nfa = (int64_t)prm.n_frames * lv[l].nf[0];
-    dim3 gf(grid_for(nfa, 128), DIM);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
-    k_kkt_faces<DIM, PER, R><<<gf, 128, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
-    int64_t nca = (int64_t)prm.n_frames * lv[l].nc;
-    k_kkt_cells<DIM, PER, R><<<grid_for(nca, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
+    int64_t tot = (int64_t)prm.n_frames * lv[l].nc;
+    prof_begin(2, lv[l].nc, st);
+    k_kkt<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
+    prof_end(2, st);
   }
 
   int n_colors() const {
@@ -902,6 +949,21 @@ struct Nso : NsoBase {
 
   void sweep(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
+  }
+
+  template <int TM>
+  void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, int has_rhs, const int o[3], int mod, const int mm[3],
+                  int64_t M, cudaStream_t st) {
+    const size_t shm = (size_t)Line<DIM>::S * Line<DIM>::NE * TM * sizeof(R);
+    auto kern = k_scgs_fwd<DIM, PER, R, TM>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+      attr = true;
+    }
+    kern<<<(unsigned)((M + TM - 1) / TM), 2 * TM, shm, st>>>(c, r, has_rhs, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                             scratch, flag);
+    count_launch();
   }
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
@@ -921,22 +983,24 @@ struct Nso : NsoBase {
     int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
     if (M == 0) return;
     int64_t tot = (int64_t)prm.n_frames * M;
+    // forward: TM colour cells per CTA (producer + consumer warp per 32);
+    // small colours use TM = 32 to spread over all SMs
     prof_begin(0, M, st);
-    k_scgs_assemble<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, o[0], o[1], o[2], mod,
-                                                                     mm[0], mm[1], mm[2], asmb); count_launch();
+    if (M >= 148 * 64 * 2) launch_fwd<64>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
+    else launch_fwd<32>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
     prof_end(0, st);
-    // latency-bound recursion: spread small colours over all SMs
-    int tpb = M >= 148 * 128 ? 128 : 32;
+    prof_begin(3, M, st);
+    {
+      int tpb = M >= 148 * 128 ? 128 : 32;
+      k_scgs_back<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
+                                                                                mm[2], (R)prm.omega, scratch, xout);
+      count_launch();
+    }
+    prof_end(3, st);
     prof_begin(1, M, st);
-    k_scgs_line<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(
-        ix, (R)L.g.h, (R)prm.dt, (R)(prm.K / prm.r), prm.n_frames, c.t0, c.Ng, c.V, o[0], o[1], o[2], mod, mm[0],
-        mm[1], mm[2],
-        (R)prm.omega, asmb, scratch, xout, flag); count_launch();
-    prof_end(1, st);
-    prof_begin(2, M, st);
     k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
                                                                    mm[1], mm[2], xout); count_launch();
-    prof_end(2, st);
+    prof_end(1, st);
 
   }
 

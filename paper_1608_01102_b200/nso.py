@@ -244,10 +244,10 @@ class StfasHierarchy:
     def profile(self, enable=True):
         _lib.check(self._L.smk_nso_profile(self._h, int(bool(enable))), "profile")
 
-    KERNELS = {0: "k_scgs_assemble", 1: "k_scgs_line", 2: "k_scgs_apply"}
+    KERNELS = {0: "k_scgs_fwd", 1: "k_scgs_apply", 2: "k_kkt", 3: "k_scgs_back"}
 
-    def profile_read(self, kind=1):
-        """(summed kernel ms, launches, cell-timesteps) for smoother kernel `kind`."""
+    def profile_read(self, kind=0):
+        """(summed kernel ms, launches, cell-timesteps) for kernel `kind` (KERNELS)."""
         ms, n, cells = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
         _lib.check(self._L.smk_nso_profile_read(self._h, int(kind), ctypes.byref(ms), ctypes.byref(n),
                                                 ctypes.byref(cells)), "profile_read")
