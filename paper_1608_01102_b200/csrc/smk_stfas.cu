@@ -251,43 +251,77 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
   return ok;
 }
 
-// The partially pivoted solve runs once per cell line (the last global pair,
-// alpha = 0, whose faces block is singular along M^-1 g); it is kept out of
-// line on a local-memory copy so its unrolled row swaps do not bloat the
-// consumer loop or pin A / X to local memory.
-template <class R, int B, int C>
-__device__ __noinline__ bool dense_solve_pivot_mem(R* T, R tiny) {
-  R A[B][B], X[B][C];
+// In-place LDL^T of a symmetric B x B matrix held in the lower triangle of T
+// (natural order, no pivoting -- used for the saddle blocks whose faces part
+// is positive definite): on exit T[r][c] (c < r) = L[r][c], dinv = 1 / d.
+template <class R, int B>
+__device__ __forceinline__ bool ldlt(R (&T)[B][B], R (&dinv)[B], R tiny) {
+  bool ok = true;
 #pragma unroll
-  for (int r = 0; r < B; ++r) {
+  for (int col = 0; col < B; ++col) {
+    const R piv = T[col][col];
+    if (!(rabs(piv) > tiny)) ok = false;
+    dinv[col] = R(1) / piv;
+    R l[B];
 #pragma unroll
-    for (int c = 0; c < B; ++c) A[r][c] = T[r * (B + C) + c];
+    for (int r = col + 1; r < B; ++r) l[r] = T[r][col] * dinv[col];
 #pragma unroll
-    for (int c = 0; c < C; ++c) X[r][c] = T[r * (B + C) + B + c];
+    for (int r = col + 1; r < B; ++r)
+#pragma unroll
+      for (int c = col + 1; c <= r; ++c) T[r][c] -= l[r] * T[c][col];
+#pragma unroll
+    for (int r = col + 1; r < B; ++r) T[r][col] = l[r];
   }
-  bool ok = dense_solve<R, B, C, true>(A, X, tiny);
-#pragma unroll
-  for (int r = 0; r < B; ++r)
-#pragma unroll
-    for (int c = 0; c < C; ++c) T[r * (B + C) + B + c] = X[r][c];
   return ok;
 }
 
-template <class R, int B, int C>
-__device__ __forceinline__ bool dense_solve_pivot(R (&A)[B][B], R (&X)[B][C], R tiny) {
-  R T[B * (B + C)];
+// b <- (L diag(d) L^T)^-1 b
+template <class R, int B>
+__device__ __forceinline__ void ldlt_solve(const R (&T)[B][B], const R (&dinv)[B], R (&b)[B]) {
+#pragma unroll
+  for (int r = 1; r < B; ++r)
+#pragma unroll
+    for (int c = 0; c < r; ++c) b[r] -= T[r][c] * b[c];
+#pragma unroll
+  for (int r = 0; r < B; ++r) b[r] *= dinv[r];
+#pragma unroll
+  for (int r = B - 2; r >= 0; --r)
+#pragma unroll
+    for (int c = r + 1; c < B; ++c) b[r] -= T[c][r] * b[c];
+}
+
+// The partially pivoted solve runs once per cell line (the last global pair,
+// alpha = 0, whose faces block is singular along M^-1 g while the saddle is
+// not); it is kept out of line on a local-memory copy so its unrolled row
+// swaps do not bloat the consumer loop.
+template <class R, int B>
+__device__ __noinline__ bool saddle_solve_pivot_mem(R* Tm, R tiny) {
+  R A[B][B], X[B][1];
 #pragma unroll
   for (int r = 0; r < B; ++r) {
 #pragma unroll
-    for (int c = 0; c < B; ++c) T[r * (B + C) + c] = A[r][c];
-#pragma unroll
-    for (int c = 0; c < C; ++c) T[r * (B + C) + B + c] = X[r][c];
+    for (int c = 0; c < B; ++c) A[r][c] = Tm[r * (B + 1) + c];
+    X[r][0] = Tm[r * (B + 1) + B];
   }
-  bool ok = dense_solve_pivot_mem<R, B, C>(T, tiny);
+  bool ok = dense_solve<R, B, 1, true>(A, X, tiny);
 #pragma unroll
-  for (int r = 0; r < B; ++r)
+  for (int r = 0; r < B; ++r) Tm[r * (B + 1) + B] = X[r][0];
+  return ok;
+}
+
+// b <- K'^-1 b for the symmetric K' held in the lower triangle of T
+template <class R, int B>
+__device__ __forceinline__ bool saddle_solve_pivot(const R (&T)[B][B], R (&b)[B], R tiny) {
+  R Tm[B * (B + 1)];
 #pragma unroll
-    for (int c = 0; c < C; ++c) X[r][c] = T[r * (B + C) + B + c];
+  for (int r = 0; r < B; ++r) {
+#pragma unroll
+    for (int c = 0; c < B; ++c) Tm[r * (B + 1) + c] = c <= r ? T[r][c] : T[c][r];
+    Tm[r * (B + 1) + B] = b[r];
+  }
+  bool ok = saddle_solve_pivot_mem<R, B>(Tm, tiny);
+#pragma unroll
+  for (int r = 0; r < B; ++r) b[r] = Tm[r * (B + 1) + B];
   return ok;
 }
 
@@ -396,16 +430,17 @@ __device__ __forceinline__ void jac_cached(R c0, R idt, const R (&v)[DIM][NbrSlo
 // neighbourhood, M_i, and hand P M_i, c_i, yv_i + M_i^T c_i and the dpbar row
 // to the consumers through an S-stage shared-memory ring (named barriers
 // FULL/EMPTY per stage); they also store the u-rows yu_i for the backward
-// pass.  Consumers run the dense elimination: per pair one (2d+1)-block solve
-// with 2d+1 right-hand sides, carrying the Schur-updated D_{i+1}, its partial
-// rhs and (P M_{i+1})^T z_i to the next pair, and store W_i (B x NF) and z_i
-// (B).  Per pair the scratch holds SE values, layout [pair][entry][m].
+// pass.  Consumers run the dense elimination (an LDL^T of each pair's
+// symmetric saddle block, see below), carrying the Schur-updated D_{i+1}, its
+// partial rhs and (P M_{i+1})^T z_i to the next pair.  Per pair the scratch
+// holds SE values (L, 1/d, z, yu), layout [pair][entry][m].
 // ---------------------------------------------------------------------------
 template <int DIM>
 struct Line {
   static constexpr int NF = 2 * DIM, B = NF + 1;
-  static constexpr int SE = B * (NF + 2);                // W, z, yu
-  static constexpr int W0 = 0, Z0 = B * NF, Y0 = B * NF + B;
+  static constexpr int NL = B * (B - 1) / 2;            // strict lower triangle of L
+  static constexpr int L0 = 0, D0 = NL, Z0 = NL + B, Y0 = NL + 2 * B;
+  static constexpr int SE = NL + 3 * B;                  // L, 1/d, z, yu
   static constexpr int NE = NF * NF + 2 * NF + 1;        // ring entry: PM, c, xr, ycell
   static constexpr int E_PM = 0, E_C = NF * NF, E_XR = NF * NF + NF, E_YC = NF * NF + 2 * NF;
   static constexpr int S = 3;                            // ring stages
@@ -518,21 +553,22 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
   }
 
   // ---------------- consumers ----------------
+  // Per pair, the saddle block K' = [[D~_i, g], [g^T, 0]] (symmetric form of
+  // the v-row / dpbar-row block) is factored K' = L diag(d) L^T in place; z_i
+  // solves K' z = [rhs; -ycell].  The coupling to the next pair enters only
+  // through Y = L^-1 [P M_{i+1}; 0]:  D~_{i+1} = D_{i+1} - Y^T diag(1/d) Y / dt^2,
+  // and the back substitution needs W_i dv = K'^-1 [-P M_{i+1} dv / dt; 0],
+  // so the pair stores (L, 1/d, z) -- no explicit W.
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
-  auto load_pm = [&](int i, R (&PM)[NF][NF]) {
-#pragma unroll
-    for (int a = 0; a < NF; ++a)
-#pragma unroll
-      for (int b = 0; b < NF; ++b) PM[a][b] = *slot(i, LN::E_PM + a * NF + b);
-  };
   // D faces block of pair ip: (PM)^T PM + [ip+1<N] P/dt^2 + alpha / wall identity
-  auto diag_block = [&](int ip, const R (&PM)[NF][NF], R (&Af)[NF][NF]) {
+  // (lower triangle)
+  auto diag_block = [&](int ip, const R (&PM)[NF][NF], R (&T)[B][B]) {
     const bool nx = ip + 1 < N;
     const R alpha = (cx.t0 + ip < cx.Ng - 1) ? cx.kr : R(0);
 #pragma unroll
     for (int a = 0; a < NF; ++a)
 #pragma unroll
-      for (int b = a; b < NF; ++b) {
+      for (int b = 0; b <= a; ++b) {
         R s = R(0);
 #pragma unroll
         for (int t = 0; t < NF; ++t) s += PM[t][a] * PM[t][b];
@@ -540,14 +576,18 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
           R pab = (a == b && !cg.wall[a] ? R(1) : R(0)) - cg.gcol[a] * cg.gcol[b] * lc.isig;
           s += pab * idt * idt;
         }
-        Af[a][b] = s;
-        Af[b][a] = s;
+        if (a == b) s += cg.wall[a] ? R(1) : alpha;
+        T[a][b] = s;
       }
-#pragma unroll
-    for (int q = 0; q < NF; ++q) Af[q][q] += cg.wall[q] ? R(1) : alpha;
   };
-  R Af[NF][NF];   // Schur-updated faces block of the current pair
-  R xr[NF];       // its partial rhs yv + M^T c
+  auto load_pm = [&](int i, R (&PM)[NF][NF]) {
+#pragma unroll
+    for (int a = 0; a < NF; ++a)
+#pragma unroll
+      for (int b = 0; b < NF; ++b) PM[a][b] = *slot(i, LN::E_PM + a * NF + b);
+  };
+  R T[B][B];      // lower triangle: D~ of the current pair, then its L
+  R xr[NF];       // partial rhs yv + M^T c of the current pair
   R sz[NF];       // (P M)^T z_{i-1}
   R ycell;        // its dpbar-row rhs
   bool ok = true;
@@ -555,7 +595,7 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
   {
     R PM[NF][NF];
     load_pm(0, PM);
-    diag_block(0, PM, Af);
+    diag_block(0, PM, T);
 #pragma unroll
     for (int a = 0; a < NF; ++a) {
       xr[a] = *slot(0, LN::E_XR + a);
@@ -563,68 +603,103 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
     }
     ycell = *slot(0, LN::E_YC);
   }
-  for (int i = 0; i < N; ++i) {
-    const bool has_next = i + 1 < N;
-    if (has_next) nb_sync(1 + (i + 1) % S, NT);   // FULL: pair i+1 ready
-    R A[B][B], X[B][C];
+  // rhs of pair i (symmetric form): faces xr - c_{i+1}/dt + sz/dt, -ycell
+  auto build_rhs = [&](int i, bool has_next, R (&b)[B]) {
 #pragma unroll
     for (int a = 0; a < NF; ++a) {
-#pragma unroll
-      for (int b = 0; b < NF; ++b) A[a][b] = Af[a][b];
-      A[a][NF] = cg.gcol[a];
-      A[NF][a] = -cg.gcol[a];
       const R cn = has_next ? *slot(i + 1, LN::E_C + a) : R(0);
       R s = cg.wall[a] ? R(0) : xr[a] - cn * idt;
-      if (i > 0) s += sz[a] * idt;
-      X[a][NF] = s;
-#pragma unroll
-      for (int b = 0; b < NF; ++b) X[a][b] = has_next ? -*slot(i + 1, LN::E_PM + a * NF + b) * idt : R(0);
-      X[NF][a] = R(0);
+      b[a] = s + sz[a] * idt;
     }
-    A[NF][NF] = R(0);
-    X[NF][NF] = ycell;
-    if (cx.t0 + i < cx.Ng - 1) ok &= dense_solve<R, B, C, false>(A, X, tinyv);
-    else ok &= dense_solve_pivot<R, B, C>(A, X, tinyv);
+    b[NF] = -ycell;
+  };
+  auto saddle = [&]() {
+#pragma unroll
+    for (int a = 0; a < NF; ++a) T[NF][a] = cg.gcol[a];
+    T[NF][NF] = R(0);
+  };
+  for (int i = 0; i < N - 1; ++i) {
+    nb_sync(1 + (i + 1) % S, NT);   // FULL: pair i+1 ready
+    R b[B], dinv[B];
+    build_rhs(i, true, b);
+    saddle();
+    ok &= ldlt<R, B>(T, dinv, tinyv);
+    ldlt_solve<R, B>(T, dinv, b);
     if (act) {
 #pragma unroll
-      for (int r = 0; r < B; ++r) {
+      for (int r = 1; r < B; ++r)
 #pragma unroll
-        for (int q = 0; q < NF; ++q) *sc(i, LN::W0 + r * NF + q) = X[r][q];
-        *sc(i, LN::Z0 + r) = X[r][NF];
+        for (int c = 0; c < r; ++c) *sc(i, LN::L0 + r * (r - 1) / 2 + c) = T[r][c];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        *sc(i, LN::D0 + r) = dinv[r];
+        *sc(i, LN::Z0 + r) = b[r];
       }
     }
-    nb_arrive(1 + S + i % S, NT);   // EMPTY: pair i released
-    if (has_next) {
-      R PM[NF][NF];
-      load_pm(i + 1, PM);
-      diag_block(i + 1, PM, Af);
-      // Schur complement of the eliminated pair: + (P M)^T W_i / dt (symmetric)
+    R PM[NF][NF];
+    load_pm(i + 1, PM);
 #pragma unroll
-      for (int a = 0; a < NF; ++a) {
+    for (int a = 0; a < NF; ++a) {
+      R s = R(0);
 #pragma unroll
-        for (int b = a; b < NF; ++b) {
-          R s = R(0);
+      for (int t = 0; t < NF; ++t) s += PM[t][a] * b[t];
+      sz[a] = s;
+      xr[a] = *slot(i + 1, LN::E_XR + a);
+    }
+    ycell = *slot(i + 1, LN::E_YC);
+    // Y = L^-1 [PM; 0], column by column (row NF starts at 0)
+    R Y[B][NF];
 #pragma unroll
-          for (int t = 0; t < NF; ++t) s += PM[t][a] * X[t][b];
-          Af[a][b] += s * idt;
-          if (b != a) Af[b][a] += s * idt;
-        }
+    for (int j = 0; j < NF; ++j) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        R s = r < NF ? PM[r][j] : R(0);
+#pragma unroll
+        for (int c = 0; c < r; ++c) s -= T[r][c] * Y[c][j];
+        Y[r][j] = s;
+      }
+    }
+    nb_arrive(1 + S + i % S, NT);   // EMPTY: pair i+1's PM is in registers; release pair i
+    diag_block(i + 1, PM, T);
+    // Schur complement of the eliminated pair: - Y^T diag(1/d) Y / dt^2
+#pragma unroll
+    for (int a = 0; a < NF; ++a)
+#pragma unroll
+      for (int c = 0; c <= a; ++c) {
         R s = R(0);
 #pragma unroll
-        for (int t = 0; t < NF; ++t) s += PM[t][a] * X[t][NF];
-        sz[a] = s;
-        xr[a] = *slot(i + 1, LN::E_XR + a);
+        for (int k = 0; k < B; ++k) s += Y[k][a] * dinv[k] * Y[k][c];
+        T[a][c] -= s * idt * idt;
       }
-      ycell = *slot(i + 1, LN::E_YC);
+  }
+  {
+    // last pair: no coupling to a next pair; only z is needed
+    const int i = N - 1;
+    R b[B];
+    build_rhs(i, false, b);
+    saddle();
+    if (cx.t0 + i < cx.Ng - 1) {
+      R dinv[B];
+      ok &= ldlt<R, B>(T, dinv, tinyv);
+      ldlt_solve<R, B>(T, dinv, b);
+    } else {
+      // alpha = 0: D~ is singular along M^-1 g; the saddle is not -> pivot
+      ok &= saddle_solve_pivot<R, B>(T, b, tinyv);
     }
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) *sc(i, LN::Z0 + r) = b[r];
+    }
+    nb_arrive(1 + S + i % S, NT);
   }
   if (act && !ok) atomicExch(flag, 1);
 }
 
-// Back substitution of one colour: dv, dpbar of pair i from the stored W_i,
-// z_i, then du, dp of pair i+1 (needs dv_{i+1}, dv_{i+2}, yu_{i+1} and
-// M_{i+1}, recomputed from V).  Writes omega * deltas to xout
-// [2 * pair + (0: u-block, 1: v-block)][entry][m].
+// Back substitution of one colour, pair i = N-1 .. 0:
+//   dv, dpbar of pair i = z_i - K'_i^-1 [-P M_{i+1} dv_{i+1} / dt; 0]  (stored
+//   L, 1/d of pair i; M_{i+1} recomputed from V), then du, dp of pair i+1
+//   from dv_{i+1}, dv_{i+2}, yu_{i+1} and the same M_{i+1} dv_{i+2}.
+// Writes omega * deltas to xout [2 * pair + (0: u-block, 1: v-block)][entry][m].
 template <int DIM, bool PER, class R>
 __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
@@ -641,17 +716,26 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   const Loc<DIM, PER> L(ix, cg.c);
   const R idt = cx.idt;
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
-  auto u_delta = [&](int i, const R (&dvi)[NF], const R (&dvn)[NF]) {
+  // t = M_i dv (M_i from the V cache of frame i)
+  auto mdot = [&](int i, const R (&dv)[NF], R (&t)[NF]) {
     R VC[DIM][NB], Mi[NF][NF];
     load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
     jac_cached<DIM, R>(cx.c0, idt, VC, cg.wall, Mi);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < NF; ++k) s += Mi[q][k] * dv[k];
+      t[q] = s;
+    }
+  };
+  // du, dp of pair i from dv_i (dvi), dv_{i+1} and t = M_i dv_{i+1}
+  auto u_delta = [&](int i, const R (&dvi)[NF], const R (&t)[NF]) {
     R a[NF];
     R ga = R(0);
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
-      R s = sc(i, LN::Y0 + q) + dvi[q] * idt;
-#pragma unroll
-      for (int t = 0; t < NF; ++t) s -= Mi[q][t] * dvn[t];
+      R s = sc(i, LN::Y0 + q) + dvi[q] * idt - t[q];
       a[q] = cg.wall[q] ? R(0) : s;
       ga += cg.gcol[q] * a[q];
     }
@@ -662,16 +746,33 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
     xo[(int64_t)NF * M] = omega * dp;
   };
   R xn[NF];   // dv of pair i+1
-#pragma unroll
-  for (int q = 0; q < NF; ++q) xn[q] = R(0);
+  R t[NF];    // M_{i+1} dv_{i+1}
   for (int i = N - 1; i >= 0; --i) {
     R xb[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) {
-      R s = sc(i, LN::Z0 + r);
+    for (int r = 0; r < B; ++r) xb[r] = sc(i, LN::Z0 + r);
+    if (i + 1 < N) {
+      mdot(i + 1, xn, t);
+      R wf[NF], w[B];
 #pragma unroll
-      for (int q = 0; q < NF; ++q) s -= sc(i, LN::W0 + r * NF + q) * xn[q];
-      xb[r] = s;
+      for (int q = 0; q < NF; ++q) wf[q] = t[q];
+      lc.projP(wf);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) w[q] = -wf[q] * idt;
+      w[NF] = R(0);
+      // K'^-1 w with the stored L, 1/d
+#pragma unroll
+      for (int r = 1; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < r; ++c) w[r] -= sc(i, LN::L0 + r * (r - 1) / 2 + c) * w[c];
+#pragma unroll
+      for (int r = 0; r < B; ++r) w[r] *= sc(i, LN::D0 + r);
+#pragma unroll
+      for (int r = B - 2; r >= 0; --r)
+#pragma unroll
+        for (int c = r + 1; c < B; ++c) w[r] -= sc(i, LN::L0 + c * (c - 1) / 2 + r) * w[c];
+#pragma unroll
+      for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
     R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
@@ -680,7 +781,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       R dvi[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
-      u_delta(i + 1, dvi, xn);
+      u_delta(i + 1, dvi, t);
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];
@@ -688,9 +789,9 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   R zero[NF];
 #pragma unroll
   for (int q = 0; q < NF; ++q) zero[q] = R(0);
-  u_delta(0, zero, xn);   // dv_0 = 0 (pinned / frozen halo)
+  mdot(0, xn, t);
+  u_delta(0, zero, t);   // dv_0 = 0 (pinned / frozen halo)
 }
-
 
 // x += omega * dx on the colour's unknowns (disjoint across cells)
 template <int DIM, bool PER, class R>
