@@ -14,6 +14,8 @@
 // take x += omega * dx.  Same-colour cells own disjoint unknowns, so the
 // apply pass is race-free and the sweep is bitwise deterministic.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -57,6 +59,7 @@ struct KktCtx {
   Ix<DIM, PER> ix;
   R c0, h, dt, kr;
   R ih, idt;       // 1/h, 1/dt (host-rounded; exact for h = 2^-k)
+  int pf;          // producer L2 prefetch mode (0 off, 1 bulk rows, 2 lines)
   int N;           // local pairs (this slab)
   int t0, Ng;      // global index of local pair 0, global pair count
   int64_t nf[3], nc;
@@ -443,7 +446,6 @@ struct Line {
   static constexpr int SE = NL + 3 * B;                  // L, 1/d, z, yu
   static constexpr int NE = NF * NF + 2 * NF + 1;        // ring entry: PM, c, xr, ycell
   static constexpr int E_PM = 0, E_C = NF * NF, E_XR = NF * NF + NF, E_YC = NF * NF + 2 * NF;
-  static constexpr int S = 3;                            // ring stages
 };
 
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -476,20 +478,107 @@ struct LineCell {
   }
 };
 
-template <int DIM, bool PER, class R, int TM>
-__global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1,
-                                                     int o2, int mod, int m0, int m1, int m2, R* __restrict__ scratch,
-                                                     int* flag) {
+// ---------------------------------------------------------------------------
+// L2 bulk prefetch of the rows a producer warp reads for pair i (3D, Neumann,
+// one warp = 32 consecutive colour cells of one (x, y) row, i.e. colour-grid
+// z extent a multiple of 32).  The warp's footprint is 74 contiguous row
+// segments (field, dx, dy) -- V and U 21 each (the NbrSlots offsets), P and
+// PBAR 5 each, the rhs rows, the guide and U_{i+1} at the own faces -- each
+// covering z in [z0 - 1, z0 + 65); lanes issue ~3 cp.async.bulk.prefetch.L2
+// each, one pair ahead of the loads.
+// ---------------------------------------------------------------------------
+// field ids: 0-2 V_a, 3-5 U_a, 6 P, 7 PBAR, 8-10 R1_a, 11-13 R3_a, 14 R2,
+// 15 R4, 16-18 vstar_a (frame i+1), 19-21 U_a (frame i+1)
+__constant__ signed char kPfRows[74][3] = {
+    {0, -1, 0}, {0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, -1}, {0, 0, 1}, {0, 1, -1}, {0, 1, 1},
+    {1, 0, -1}, {1, 0, 0}, {1, 0, 1}, {1, 0, 2}, {1, -1, 0}, {1, 1, 0}, {1, -1, 1}, {1, 1, 1},
+    {2, 0, 0}, {2, -1, 0}, {2, 1, 0}, {2, 0, -1}, {2, 0, 1},
+    {3, -1, 0}, {3, 0, 0}, {3, 1, 0}, {3, 2, 0}, {3, 0, -1}, {3, 0, 1}, {3, 1, -1}, {3, 1, 1},
+    {4, 0, -1}, {4, 0, 0}, {4, 0, 1}, {4, 0, 2}, {4, -1, 0}, {4, 1, 0}, {4, -1, 1}, {4, 1, 1},
+    {5, 0, 0}, {5, -1, 0}, {5, 1, 0}, {5, 0, -1}, {5, 0, 1},
+    {6, 0, 0}, {6, -1, 0}, {6, 1, 0}, {6, 0, -1}, {6, 0, 1},
+    {7, 0, 0}, {7, -1, 0}, {7, 1, 0}, {7, 0, -1}, {7, 0, 1},
+    {8, 0, 0}, {8, 1, 0}, {9, 0, 0}, {9, 0, 1}, {10, 0, 0},
+    {11, 0, 0}, {11, 1, 0}, {12, 0, 0}, {12, 0, 1}, {13, 0, 0},
+    {14, 0, 0}, {15, 0, 0},
+    {16, 0, 0}, {16, 1, 0}, {17, 0, 0}, {17, 0, 1}, {18, 0, 0},
+    {19, 0, 0}, {19, 1, 0}, {20, 0, 0}, {20, 0, 1}, {21, 0, 0}};
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+template <bool PER, class R>
+__device__ __forceinline__ void prefetch_pair_rows(const KktCtx<3, PER, R>& cx, const ResP<R>& rhs, bool has_rhs,
+                                                   int i, int x, int y, int z0, int lane) {
+  const auto& ix = cx.ix;
+  const bool inner = cx.inner(i) && i + 1 < cx.N;
+  for (int e = lane; e < 74; e += 32) {
+    const int f = kPfRows[e][0];
+    if (!has_rhs && f >= 8 && f <= 15) continue;
+    if (!inner && f >= 16) continue;
+    const int xx = x + kPfRows[e][1], yy = y + kPfRows[e][2];
+    const R* base;
+    int e0, e1, e2;   // extents of the array along the three axes
+    if (f == 6 || f == 7 || f == 14 || f == 15) {
+      e0 = ix.n0; e1 = ix.n1; e2 = ix.n2;
+      base = f == 6 ? cx.P : (f == 7 ? cx.PB : (f == 14 ? rhs.R2 : rhs.R4));
+      base += (int64_t)i * cx.nc;
+    } else {
+      const int k = f < 6 ? f % 3 : (f < 14 ? (f - 8) % 3 : (f - 16) % 3);
+      e0 = ix.fe(k, 0); e1 = ix.fe(k, 1); e2 = ix.fe(k, 2);
+      int64_t fr = i;
+      if (f < 3) base = cx.V.c[k];
+      else if (f < 6) base = cx.U.c[k];
+      else if (f < 11) base = rhs.R1[k];
+      else if (f < 14) base = rhs.R3[k];
+      else if (f < 19) { base = cx.vs.c[k]; fr = i + 1; }
+      else { base = cx.U.c[k]; fr = i + 1; }
+      base += fr * cx.nf[k];
+    }
+    if (xx < 0 || yy < 0 || xx >= e0 || yy >= e1) continue;
+    const R* row = base + ((int64_t)xx * e1 + yy) * e2;
+    const int zlo = max(z0 - 1, 0), zhi = min(z0 + 65, e2);
+    const uintptr_t a = reinterpret_cast<uintptr_t>(row + zlo) & ~uintptr_t(15);
+    const uintptr_t b = reinterpret_cast<uintptr_t>(row + zhi);
+    if (cx.pf == 1) {
+      const unsigned bytes = (unsigned)((b - a) & ~uintptr_t(15));
+      if (bytes) bulk_prefetch_l2(reinterpret_cast<const void*>(a), bytes);
+    } else {
+      for (uintptr_t q = a & ~uintptr_t(127); q < b; q += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+    }
+  }
+}
+
+// ring stages for P producer groups: a multiple of P, at least 3
+__host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P == 2 ? 4 : P); }
+
+// k_scgs_fwd<TM, P>: TM cells per CTA, P producer groups of TM threads
+// (group p builds pairs i = p mod P, so the coarse levels -- few cells, long
+// time lines -- get P-fold producer parallelism), one consumer group.
+// resident CTAs per SM the register budget is sized for
+__host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
+  return (P == 1 ? 4 : (P == 2 ? 5 : 2)) / (esz == 8 ? 2 : 1) > 0 ? (P == 1 ? 4 : (P == 2 ? 5 : 2)) / (esz == 8 ? 2 : 1)
+                                                                   : 1;
+}
+
+template <int DIM, bool PER, class R, int TM, int P>
+__global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R)))
+    k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1, int o2, int mod, int m0, int m1,
+               int m2, R* __restrict__ scratch, int* flag) {
   using LN = Line<DIM>;
-  constexpr int NF = LN::NF, B = LN::B, C = NF + 1, NB = NbrSlots<DIM>::NB, NE = LN::NE, S = LN::S;
-  constexpr int NT = 2 * TM;
+  constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB, NE = LN::NE;
+  constexpr int S = ring_stages(P);
+  constexpr int NT = 2 * TM;   // threads per named barrier: one producer group + the consumers
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* ring = reinterpret_cast<R*>(smem_raw);   // [S][NE][TM]
   const auto& ix = cx.ix;
   const int N = cx.N;
   const int64_t M = (int64_t)m0 * m1 * m2;
-  const bool producer = threadIdx.x < TM;
-  const int lane = producer ? threadIdx.x : threadIdx.x - TM;
+  const int grp = threadIdx.x / TM;           // 0..P-1 producers, P consumers
+  const bool producer = grp < P;
+  const int lane = threadIdx.x - grp * TM;
   const int64_t m = (int64_t)blockIdx.x * TM + lane;
   const bool act = m < M;   // inactive threads still take part in every barrier
   const LineCell<DIM, PER, R> lc(ix, cx.h, act ? m : 0, o0, o1, o2, mod, m1, m2);
@@ -502,12 +591,29 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
   if (producer) {
     const Loc<DIM, PER> L(ix, cg.c);
     const bool hr = has_rhs != 0;
-    R vp[NF];   // V_{i-1} at the own faces
+    R vp[NF];   // V_{i-1} at the own faces (carried when one group builds every pair)
+    if (P == 1) {
 #pragma unroll
-    for (int q = 0; q < NF; ++q) vp[q] = act ? cx.v0.c[q >> 1][L.of[q]] : R(0);
-    for (int i = 0; i < N; ++i) {
+      for (int q = 0; q < NF; ++q) vp[q] = act ? cx.v0.c[q >> 1][L.of[q]] : R(0);
+    }
+    // one-pair-ahead L2 prefetch of the warp's rows (3D Neumann, P == 1)
+    const bool pf = DIM == 3 && !PER && P == 1 && m2 % 32 == 0 && cx.pf != 0;
+    const int wlane = threadIdx.x & 31;
+    const int z0 = __shfl_sync(0xffffffffu, cg.c[2], 0);
+    if constexpr (DIM == 3 && !PER) {
+      if (pf && act) prefetch_pair_rows<PER, R>(cx, rhs, hr, 0, cg.c[0], cg.c[1], z0, wlane);
+    }
+    for (int i = grp; i < N; i += P) {
       if (i >= S) nb_sync(1 + S + i % S, NT);   // EMPTY: the consumers released pair i - S
+      if constexpr (DIM == 3 && !PER) {
+        if (pf && act && i + 1 < N) prefetch_pair_rows<PER, R>(cx, rhs, hr, i + 1, cg.c[0], cg.c[1], z0, wlane);
+      }
       if (act) {
+        if (P > 1) {
+          const Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
+#pragma unroll
+          for (int q = 0; q < NF; ++q) vp[q] = Vp.c[q >> 1][L.of[q]];
+        }
         R VC[DIM][NB], UC[DIM][NB];
         R yu[B], yv[B];
         load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
@@ -519,8 +625,10 @@ __global__ void __launch_bounds__(2 * TM, (sizeof(R) == 8 ? 128 : 192) / TM) k_s
           yv[q] = -yv[q];
           *sc(i, LN::Y0 + q) = yu[q];
         }
+        if (P == 1) {
 #pragma unroll
-        for (int q = 0; q < NF; ++q) vp[q] = VC[q >> 1][(q & 1) + 1];
+          for (int q = 0; q < NF; ++q) vp[q] = VC[q >> 1][(q & 1) + 1];
+        }
         R Mx[NF][NF], cv[NF];
         jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
 #pragma unroll
@@ -913,7 +1021,21 @@ struct Nso : NsoBase {
     return (R*)p;
   }
 
+  // forward-kernel shape thresholds (colour cells): >= fwd_big -> TM 64 / P 1,
+  // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
+  // overrides them (tuning runs only).
+  int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 64 * 4;
+  int pf_mode = 0;   // SMK_PF (tuning)
+
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
+    if (const char* e = getenv("SMK_PF")) pf_mode = atoi(e);
+    if (const char* e = getenv("SMK_FWD_THRESH")) {
+      long long a = 0, b = 0;
+      if (sscanf(e, "%lld,%lld", &a, &b) == 2) {
+        fwd_big = a;
+        fwd_mid = b;
+      }
+    }
     int want = p.n_levels < 1 ? 1 : p.n_levels;
     Geo cur = g;
     for (int l = 0; l < want; ++l) {
@@ -1007,6 +1129,7 @@ struct Nso : NsoBase {
     c.dt = (R)prm.dt;
     c.ih = (R)(1.0 / L.g.h);
     c.idt = (R)(1.0 / prm.dt);
+    c.pf = pf_mode;
     c.kr = (R)(prm.K / prm.r);
     c.N = prm.n_frames;
     for (int k = 0; k < 3; ++k) c.nf[k] = L.nf[k];
@@ -1052,18 +1175,18 @@ struct Nso : NsoBase {
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
   }
 
-  template <int TM>
+  template <int TM, int P>
   void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, int has_rhs, const int o[3], int mod, const int mm[3],
                   int64_t M, cudaStream_t st) {
-    const size_t shm = (size_t)Line<DIM>::S * Line<DIM>::NE * TM * sizeof(R);
-    auto kern = k_scgs_fwd<DIM, PER, R, TM>;
+    const size_t shm = (size_t)ring_stages(P) * Line<DIM>::NE * TM * sizeof(R);
+    auto kern = k_scgs_fwd<DIM, PER, R, TM, P>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
       attr = true;
     }
-    kern<<<(unsigned)((M + TM - 1) / TM), 2 * TM, shm, st>>>(c, r, has_rhs, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                             scratch, flag);
+    kern<<<(unsigned)((M + TM - 1) / TM), (P + 1) * TM, shm, st>>>(c, r, has_rhs, o[0], o[1], o[2], mod, mm[0], mm[1],
+                                                                   mm[2], scratch, flag);
     count_launch();
   }
 
@@ -1087,8 +1210,12 @@ struct Nso : NsoBase {
     // forward: TM colour cells per CTA (producer + consumer warp per 32);
     // small colours use TM = 32 to spread over all SMs
     prof_begin(0, M, st);
-    if (M >= 148 * 64 * 2) launch_fwd<64>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
-    else launch_fwd<32>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
+    // colour cells per SM decide the shape: many -> one producer group
+    // (throughput), few -> more producer groups per cell (latency)
+    int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
+    if (shape == 0) launch_fwd<64, 1>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
+    else if (shape == 1) launch_fwd<32, 2>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
+    else launch_fwd<32, 4>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
     prof_end(0, st);
     prof_begin(3, M, st);
     {
