@@ -59,7 +59,6 @@ struct KktCtx {
   Ix<DIM, PER> ix;
   R c0, h, dt, kr;
   R ih, idt;       // 1/h, 1/dt (host-rounded; exact for h = 2^-k)
-  int pf;          // producer L2 prefetch mode (0 off, 1 bulk rows, 2 lines)
   int N;           // local pairs (this slab)
   int t0, Ng;      // global index of local pair 0, global pair count
   int64_t nf[3], nc;
@@ -84,21 +83,43 @@ struct KktCtx {
 // (the smoother assembles only unknown rows).  Same term order as
 // oracle/stfas.py kkt_residual; 1/h and 1/dt are multiplied, not divided.
 // ---------------------------------------------------------------------------
-template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS>
+template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS, bool HR>
 __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const Loc<DIM, PER>& L,
                                           const bool (&wall)[2 * DIM], int i,
                                           const R (&VC)[DIM][NbrSlots<DIM>::NB],
                                           const R (&UC)[DIM][NbrSlots<DIM>::NB], const R (&vp)[2 * DIM],
-                                          const ResP<R>& rhs, bool has_rhs, R (&yu)[2 * DIM + 1],
+                                          const ResP<R>& rhs, R (&yu)[2 * DIM + 1],
                                           R (&yv)[2 * DIM + 1]) {
   constexpr int NF = 2 * DIM;
   const auto& ix = cx.ix;
   const R* Pi = cx.P + (int64_t)i * cx.nc;
   const R* PBi = cx.PB + (int64_t)i * cx.nc;
-  const R pc = Pi[L.co], pbc = PBi[L.co];
   const bool inner = cx.inner(i);
   const Face3<R> Un = inner ? cx.u_next(i) : Face3<R>{};
   const Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Face3<R>{};
+  // gather every scalar input first, so all of the pair's loads are in
+  // flight together (one memory latency per pair, not one per face)
+  const R pc = Pi[L.co], pbc = PBi[L.co];
+  R pn[NF], pbn[NF], vsv[NF], unv[NF], r1v[NF], r3v[NF];
+  static_for<NF>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    constexpr int j = q >> 1, sd = q & 1;
+    constexpr int d = sd ? 1 : -1;
+    const bool on = (BOTH || sd == 0);
+    const int64_t oo = (int64_t)i * cx.nf[j] + L.of[q];
+    pn[q] = (on && !wall[q]) ? L.cell(ix, Pi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
+    pbn[q] = (on && !wall[q]) ? L.cell(ix, PBi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
+    vsv[q] = (on && inner && !wall[q]) ? Vs.c[j][L.of[q]] : R(0);
+    unv[q] = (on && inner && !wall[q]) ? Un.c[j][L.of[q]] : R(0);
+    r1v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R1[j][oo] : R(0);
+    r3v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R3[j][oo] : R(0);
+  });
+  R r2c = R(0), r4c = R(0);
+  if (HR) {
+    const int64_t o = (int64_t)i * cx.nc + L.co;
+    r4c = rhs.R4[o];
+    r2c = rhs.R2[o];
+  }
   static_for<NF>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
     constexpr int j = q >> 1, sd = q & 1;
@@ -106,28 +127,22 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
       yu[q] = R(0);
       yv[q] = R(0);
     } else {
-      const int64_t oo = (int64_t)i * cx.nf[j] + L.of[q];
       if (wall[q]) {
-        yu[q] = (WALLRHS && has_rhs) ? R(0) - rhs.R3[j][oo] : R(0);
-        yv[q] = (WALLRHS && has_rhs) ? R(0) - rhs.R1[j][oo] : R(0);
+        yu[q] = (WALLRHS && HR) ? R(0) - r3v[q] : R(0);
+        yv[q] = (WALLRHS && HR) ? R(0) - r1v[q] : R(0);
       } else {
-        // the other cell of the face (exists: the face is not a wall)
-        const R pn = L.cell(ix, Pi, j == 0 ? (sd ? 1 : -1) : 0, j == 1 ? (sd ? 1 : -1) : 0,
-                            j == 2 ? (sd ? 1 : -1) : 0);
-        const R pbn = L.cell(ix, PBi, j == 0 ? (sd ? 1 : -1) : 0, j == 1 ? (sd ? 1 : -1) : 0,
-                             j == 2 ? (sd ? 1 : -1) : 0);
-        const R gp = sd ? (pn - pc) * cx.ih : (pc - pn) * cx.ih;
-        const R gpb = sd ? (pbn - pbc) * cx.ih : (pbc - pbn) * cx.ih;
+        const R gp = sd ? (pn[q] - pc) * cx.ih : (pc - pn[q]) * cx.ih;
+        const R gpb = sd ? (pbn[q] - pbc) * cx.ih : (pbc - pbn[q]) * cx.ih;
         const R vf = VC[j][sd + 1], uf = UC[j][sd + 1];
         const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC, VC, true, true);
         R a = (((vf - vp[q]) * cx.idt + adv) - uf) + gp;
         R t1 = R(0);
-        if (inner) t1 = cx.kr * (vf - Vs.c[j][L.of[q]]) - Un.c[j][L.of[q]] * cx.idt;
+        if (inner) t1 = cx.kr * (vf - vsv[q]) - unv[q] * cx.idt;
         const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC, UC) - S_cached<DIM, j, sd, R>(cx.c0, VC, UC, true, true);
         R b = ((t1 + uf * cx.idt) + jt) + gpb;
-        if (has_rhs) {
-          a -= rhs.R3[j][oo];
-          b -= rhs.R1[j][oo];
+        if (HR) {
+          a -= r3v[q];
+          b -= r1v[q];
         }
         yu[q] = a;
         yv[q] = b;
@@ -142,10 +157,9 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
     dv = (k == 0) ? a : dv + a;
     du = (k == 0) ? b : du + b;
   }
-  if (has_rhs) {
-    const int64_t o = (int64_t)i * cx.nc + L.co;
-    du -= rhs.R4[o];
-    dv -= rhs.R2[o];
+  if (HR) {
+    du -= r4c;
+    dv -= r2c;
   }
   yu[NF] = du;
   yv[NF] = dv;
@@ -156,8 +170,8 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
 // upper wall face of the last cell along each axis (0 - rhs).  Neighbour
 // values come from the register caches (every V / U value the cell's faces
 // need is read once per thread, through L1).
-template <int DIM, bool PER, class R>
-__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, ResP<R> out) {
+template <int DIM, bool PER, class R, bool HR>
+__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out) {
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
@@ -180,7 +194,7 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
 #pragma unroll
     for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
     R yu[B], yv[B];
-    pair_rows<DIM, PER, R, false, true>(cx, L, wall, i, VC, UC, vp, rhs, has_rhs != 0, yu, yv);
+    pair_rows<DIM, PER, R, false, true, HR>(cx, L, wall, i, VC, UC, vp, rhs, yu, yv);
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
       const int64_t o = (int64_t)i * cx.nf[k] + L.of[2 * k];
@@ -188,8 +202,8 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
       out.R1[k][o] = yv[2 * k];
       if (!PER && wall[2 * k + 1]) {
         const int64_t ou = (int64_t)i * cx.nf[k] + L.of[2 * k + 1];
-        out.R3[k][ou] = has_rhs ? R(0) - rhs.R3[k][ou] : R(0);
-        out.R1[k][ou] = has_rhs ? R(0) - rhs.R1[k][ou] : R(0);
+        out.R3[k][ou] = HR ? R(0) - rhs.R3[k][ou] : R(0);
+        out.R1[k][ou] = HR ? R(0) - rhs.R1[k][ou] : R(0);
       }
     }
     const int64_t oc = (int64_t)i * nc + L.co;
@@ -430,10 +444,9 @@ __device__ __forceinline__ void jac_cached(R c0, R idt, const R (&v)[DIM][NbrSlo
 // [0, TM/32) are producers, [TM/32, 2TM/32) consumers, one thread of each per
 // cell.  Producers stream the state (all the HBM reads of the pass): the
 // -(f - rhs) rows of pair i from register caches of the cell's
-// neighbourhood, M_i, and hand P M_i, c_i, yv_i + M_i^T c_i and the dpbar row
-// to the consumers through an S-stage shared-memory ring (named barriers
-// FULL/EMPTY per stage); they also store the u-rows yu_i for the backward
-// pass.  Consumers run the dense elimination (an LDL^T of each pair's
+// neighbourhood, and hand the rows and the V stencil values behind M_i to the
+// consumers through an S-stage shared-memory ring (named barriers FULL/EMPTY
+// per stage); they also store the u-rows yu_i for the backward pass.  Consumers run the dense elimination (an LDL^T of each pair's
 // symmetric saddle block, see below), carrying the Schur-updated D_{i+1}, its
 // partial rhs and (P M_{i+1})^T z_i to the next pair.  Per pair the scratch
 // holds SE values (L, 1/d, z, yu), layout [pair][entry][m].
@@ -444,8 +457,9 @@ struct Line {
   static constexpr int NL = B * (B - 1) / 2;            // strict lower triangle of L
   static constexpr int L0 = 0, D0 = NL, Z0 = NL + B, Y0 = NL + 2 * B;
   static constexpr int SE = NL + 3 * B;                  // L, 1/d, z, yu
-  static constexpr int NE = NF * NF + 2 * NF + 1;        // ring entry: PM, c, xr, ycell
-  static constexpr int E_PM = 0, E_C = NF * NF, E_XR = NF * NF + NF, E_YC = NF * NF + 2 * NF;
+  static constexpr int NV = DIM * NbrSlots<DIM>::NB;     // V stencil values behind M
+  static constexpr int NE = 2 * B + NV;                  // ring entry: yu, yv, V stencil
+  static constexpr int E_YU = 0, E_YV = B, E_VS = 2 * B;
 };
 
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -478,79 +492,6 @@ struct LineCell {
   }
 };
 
-// ---------------------------------------------------------------------------
-// L2 bulk prefetch of the rows a producer warp reads for pair i (3D, Neumann,
-// one warp = 32 consecutive colour cells of one (x, y) row, i.e. colour-grid
-// z extent a multiple of 32).  The warp's footprint is 74 contiguous row
-// segments (field, dx, dy) -- V and U 21 each (the NbrSlots offsets), P and
-// PBAR 5 each, the rhs rows, the guide and U_{i+1} at the own faces -- each
-// covering z in [z0 - 1, z0 + 65); lanes issue ~3 cp.async.bulk.prefetch.L2
-// each, one pair ahead of the loads.
-// ---------------------------------------------------------------------------
-// field ids: 0-2 V_a, 3-5 U_a, 6 P, 7 PBAR, 8-10 R1_a, 11-13 R3_a, 14 R2,
-// 15 R4, 16-18 vstar_a (frame i+1), 19-21 U_a (frame i+1)
-__constant__ signed char kPfRows[74][3] = {
-    {0, -1, 0}, {0, 0, 0}, {0, 1, 0}, {0, 2, 0}, {0, 0, -1}, {0, 0, 1}, {0, 1, -1}, {0, 1, 1},
-    {1, 0, -1}, {1, 0, 0}, {1, 0, 1}, {1, 0, 2}, {1, -1, 0}, {1, 1, 0}, {1, -1, 1}, {1, 1, 1},
-    {2, 0, 0}, {2, -1, 0}, {2, 1, 0}, {2, 0, -1}, {2, 0, 1},
-    {3, -1, 0}, {3, 0, 0}, {3, 1, 0}, {3, 2, 0}, {3, 0, -1}, {3, 0, 1}, {3, 1, -1}, {3, 1, 1},
-    {4, 0, -1}, {4, 0, 0}, {4, 0, 1}, {4, 0, 2}, {4, -1, 0}, {4, 1, 0}, {4, -1, 1}, {4, 1, 1},
-    {5, 0, 0}, {5, -1, 0}, {5, 1, 0}, {5, 0, -1}, {5, 0, 1},
-    {6, 0, 0}, {6, -1, 0}, {6, 1, 0}, {6, 0, -1}, {6, 0, 1},
-    {7, 0, 0}, {7, -1, 0}, {7, 1, 0}, {7, 0, -1}, {7, 0, 1},
-    {8, 0, 0}, {8, 1, 0}, {9, 0, 0}, {9, 0, 1}, {10, 0, 0},
-    {11, 0, 0}, {11, 1, 0}, {12, 0, 0}, {12, 0, 1}, {13, 0, 0},
-    {14, 0, 0}, {15, 0, 0},
-    {16, 0, 0}, {16, 1, 0}, {17, 0, 0}, {17, 0, 1}, {18, 0, 0},
-    {19, 0, 0}, {19, 1, 0}, {20, 0, 0}, {20, 0, 1}, {21, 0, 0}};
-
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-template <bool PER, class R>
-__device__ __forceinline__ void prefetch_pair_rows(const KktCtx<3, PER, R>& cx, const ResP<R>& rhs, bool has_rhs,
-                                                   int i, int x, int y, int z0, int lane) {
-  const auto& ix = cx.ix;
-  const bool inner = cx.inner(i) && i + 1 < cx.N;
-  for (int e = lane; e < 74; e += 32) {
-    const int f = kPfRows[e][0];
-    if (!has_rhs && f >= 8 && f <= 15) continue;
-    if (!inner && f >= 16) continue;
-    const int xx = x + kPfRows[e][1], yy = y + kPfRows[e][2];
-    const R* base;
-    int e0, e1, e2;   // extents of the array along the three axes
-    if (f == 6 || f == 7 || f == 14 || f == 15) {
-      e0 = ix.n0; e1 = ix.n1; e2 = ix.n2;
-      base = f == 6 ? cx.P : (f == 7 ? cx.PB : (f == 14 ? rhs.R2 : rhs.R4));
-      base += (int64_t)i * cx.nc;
-    } else {
-      const int k = f < 6 ? f % 3 : (f < 14 ? (f - 8) % 3 : (f - 16) % 3);
-      e0 = ix.fe(k, 0); e1 = ix.fe(k, 1); e2 = ix.fe(k, 2);
-      int64_t fr = i;
-      if (f < 3) base = cx.V.c[k];
-      else if (f < 6) base = cx.U.c[k];
-      else if (f < 11) base = rhs.R1[k];
-      else if (f < 14) base = rhs.R3[k];
-      else if (f < 19) { base = cx.vs.c[k]; fr = i + 1; }
-      else { base = cx.U.c[k]; fr = i + 1; }
-      base += fr * cx.nf[k];
-    }
-    if (xx < 0 || yy < 0 || xx >= e0 || yy >= e1) continue;
-    const R* row = base + ((int64_t)xx * e1 + yy) * e2;
-    const int zlo = max(z0 - 1, 0), zhi = min(z0 + 65, e2);
-    const uintptr_t a = reinterpret_cast<uintptr_t>(row + zlo) & ~uintptr_t(15);
-    const uintptr_t b = reinterpret_cast<uintptr_t>(row + zhi);
-    if (cx.pf == 1) {
-      const unsigned bytes = (unsigned)((b - a) & ~uintptr_t(15));
-      if (bytes) bulk_prefetch_l2(reinterpret_cast<const void*>(a), bytes);
-    } else {
-      for (uintptr_t q = a & ~uintptr_t(127); q < b; q += 128)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
-    }
-  }
-}
-
 // ring stages for P producer groups: a multiple of P, at least 3
 __host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P == 2 ? 4 : P); }
 
@@ -563,9 +504,9 @@ __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
                                                                    : 1;
 }
 
-template <int DIM, bool PER, class R, int TM, int P>
+template <int DIM, bool PER, class R, int TM, int P, bool HR>
 __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R)))
-    k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int has_rhs, int o0, int o1, int o2, int mod, int m0, int m1,
+    k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int o0, int o1, int o2, int mod, int m0, int m1,
                int m2, R* __restrict__ scratch, int* flag) {
   using LN = Line<DIM>;
   constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB, NE = LN::NE;
@@ -590,24 +531,13 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 
   if (producer) {
     const Loc<DIM, PER> L(ix, cg.c);
-    const bool hr = has_rhs != 0;
     R vp[NF];   // V_{i-1} at the own faces (carried when one group builds every pair)
     if (P == 1) {
 #pragma unroll
       for (int q = 0; q < NF; ++q) vp[q] = act ? cx.v0.c[q >> 1][L.of[q]] : R(0);
     }
-    // one-pair-ahead L2 prefetch of the warp's rows (3D Neumann, P == 1)
-    const bool pf = DIM == 3 && !PER && P == 1 && m2 % 32 == 0 && cx.pf != 0;
-    const int wlane = threadIdx.x & 31;
-    const int z0 = __shfl_sync(0xffffffffu, cg.c[2], 0);
-    if constexpr (DIM == 3 && !PER) {
-      if (pf && act) prefetch_pair_rows<PER, R>(cx, rhs, hr, 0, cg.c[0], cg.c[1], z0, wlane);
-    }
     for (int i = grp; i < N; i += P) {
       if (i >= S) nb_sync(1 + S + i % S, NT);   // EMPTY: the consumers released pair i - S
-      if constexpr (DIM == 3 && !PER) {
-        if (pf && act && i + 1 < N) prefetch_pair_rows<PER, R>(cx, rhs, hr, i + 1, cg.c[0], cg.c[1], z0, wlane);
-      }
       if (act) {
         if (P > 1) {
           const Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
@@ -618,7 +548,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         R yu[B], yv[B];
         load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
         load_nbr<DIM, PER, R>(ix, L, frame_of(cx.U, i, cx.nf), UC);
-        pair_rows<DIM, PER, R, true, false>(cx, L, cg.wall, i, VC, UC, vp, rhs, hr, yu, yv);
+        pair_rows<DIM, PER, R, true, false, HR>(cx, L, cg.wall, i, VC, UC, vp, rhs, yu, yv);
 #pragma unroll
         for (int q = 0; q < B; ++q) {
           yu[q] = -yu[q];
@@ -629,31 +559,15 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 #pragma unroll
           for (int q = 0; q < NF; ++q) vp[q] = VC[q >> 1][(q & 1) + 1];
         }
-        R Mx[NF][NF], cv[NF];
-        jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
 #pragma unroll
-        for (int q = 0; q < NF; ++q) cv[q] = yu[q];
-        lc.projP(cv);
-#pragma unroll
-        for (int q = 0; q < NF; ++q) cv[q] += cg.gcol[q] * yu[NF] * lc.isig;
-#pragma unroll
-        for (int a = 0; a < NF; ++a) {
-          R s = yv[a];
-#pragma unroll
-          for (int t = 0; t < NF; ++t) s += Mx[t][a] * cv[t];
-          *slot(i, LN::E_XR + a) = s;
-          *slot(i, LN::E_C + a) = cv[a];
+        for (int q = 0; q < B; ++q) {
+          *slot(i, LN::E_YU + q) = yu[q];
+          *slot(i, LN::E_YV + q) = yv[q];
         }
-        *slot(i, LN::E_YC) = yv[NF];
 #pragma unroll
-        for (int b = 0; b < NF; ++b) {
-          R col[NF];
+        for (int a = 0; a < DIM; ++a)
 #pragma unroll
-          for (int a = 0; a < NF; ++a) col[a] = Mx[a][b];
-          lc.projP(col);
-#pragma unroll
-          for (int a = 0; a < NF; ++a) *slot(i, LN::E_PM + a * NF + b) = col[a];
-        }
+          for (int sl = 0; sl < NB; ++sl) *slot(i, LN::E_VS + a * NB + sl) = VC[a][sl];
       }
       nb_arrive(1 + i % S, NT);   // FULL
     }
@@ -688,11 +602,42 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         T[a][b] = s;
       }
   };
-  auto load_pm = [&](int i, R (&PM)[NF][NF]) {
+  // c = P yu + g yu_p / sigma of pair i (from the ring)
+  auto c_of = [&](int i, R (&cv)[NF]) {
 #pragma unroll
-    for (int a = 0; a < NF; ++a)
+    for (int q = 0; q < NF; ++q) cv[q] = *slot(i, LN::E_YU + q);
+    lc.projP(cv);
+    const R yp = *slot(i, LN::E_YU + NF);
 #pragma unroll
-      for (int b = 0; b < NF; ++b) PM[a][b] = *slot(i, LN::E_PM + a * NF + b);
+    for (int q = 0; q < NF; ++q) cv[q] += cg.gcol[q] * yp * lc.isig;
+  };
+  // M_i from the V stencil, then P M_i, the partial rhs yv + M^T c and the
+  // dpbar-row rhs of pair i
+  auto mats_of = [&](int i, const R (&cv)[NF], R (&PM)[NF][NF], R (&xrr)[NF], R& yc) {
+    R VC[DIM][NB];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a)
+#pragma unroll
+      for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(i, LN::E_VS + a * NB + sl);
+    R Mx[NF][NF];
+    jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
+#pragma unroll
+    for (int a = 0; a < NF; ++a) {
+      R s = *slot(i, LN::E_YV + a);
+#pragma unroll
+      for (int t = 0; t < NF; ++t) s += Mx[t][a] * cv[t];
+      xrr[a] = s;
+    }
+    yc = *slot(i, LN::E_YV + NF);
+#pragma unroll
+    for (int b = 0; b < NF; ++b) {
+      R col[NF];
+#pragma unroll
+      for (int a = 0; a < NF; ++a) col[a] = Mx[a][b];
+      lc.projP(col);
+#pragma unroll
+      for (int a = 0; a < NF; ++a) PM[a][b] = col[a];
+    }
   };
   R T[B][B];      // lower triangle: D~ of the current pair, then its L
   R xr[NF];       // partial rhs yv + M^T c of the current pair
@@ -701,22 +646,18 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   bool ok = true;
   nb_sync(1 + 0, NT);
   {
-    R PM[NF][NF];
-    load_pm(0, PM);
+    R PM[NF][NF], cv[NF];
+    c_of(0, cv);
+    mats_of(0, cv, PM, xr, ycell);
     diag_block(0, PM, T);
 #pragma unroll
-    for (int a = 0; a < NF; ++a) {
-      xr[a] = *slot(0, LN::E_XR + a);
-      sz[a] = R(0);
-    }
-    ycell = *slot(0, LN::E_YC);
+    for (int a = 0; a < NF; ++a) sz[a] = R(0);
   }
   // rhs of pair i (symmetric form): faces xr - c_{i+1}/dt + sz/dt, -ycell
-  auto build_rhs = [&](int i, bool has_next, R (&b)[B]) {
+  auto build_rhs = [&](const R (&cn)[NF], R (&b)[B]) {
 #pragma unroll
     for (int a = 0; a < NF; ++a) {
-      const R cn = has_next ? *slot(i + 1, LN::E_C + a) : R(0);
-      R s = cg.wall[a] ? R(0) : xr[a] - cn * idt;
+      R s = cg.wall[a] ? R(0) : xr[a] - cn[a] * idt;
       b[a] = s + sz[a] * idt;
     }
     b[NF] = -ycell;
@@ -727,9 +668,11 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     T[NF][NF] = R(0);
   };
   for (int i = 0; i < N - 1; ++i) {
+    nb_arrive(1 + S + i % S, NT);   // EMPTY: pair i's stage was consumed at step i-1
     nb_sync(1 + (i + 1) % S, NT);   // FULL: pair i+1 ready
-    R b[B], dinv[B];
-    build_rhs(i, true, b);
+    R b[B], dinv[B], cn[NF];
+    c_of(i + 1, cn);
+    build_rhs(cn, b);
     saddle();
     ok &= ldlt<R, B>(T, dinv, tinyv);
     ldlt_solve<R, B>(T, dinv, b);
@@ -745,16 +688,14 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
       }
     }
     R PM[NF][NF];
-    load_pm(i + 1, PM);
+    mats_of(i + 1, cn, PM, xr, ycell);
 #pragma unroll
     for (int a = 0; a < NF; ++a) {
       R s = R(0);
 #pragma unroll
       for (int t = 0; t < NF; ++t) s += PM[t][a] * b[t];
       sz[a] = s;
-      xr[a] = *slot(i + 1, LN::E_XR + a);
     }
-    ycell = *slot(i + 1, LN::E_YC);
     // Y = L^-1 [PM; 0], column by column (row NF starts at 0)
     R Y[B][NF];
 #pragma unroll
@@ -767,7 +708,6 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         Y[r][j] = s;
       }
     }
-    nb_arrive(1 + S + i % S, NT);   // EMPTY: pair i+1's PM is in registers; release pair i
     diag_block(i + 1, PM, T);
     // Schur complement of the eliminated pair: - Y^T diag(1/d) Y / dt^2
 #pragma unroll
@@ -783,8 +723,10 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   {
     // last pair: no coupling to a next pair; only z is needed
     const int i = N - 1;
-    R b[B];
-    build_rhs(i, false, b);
+    R b[B], cn[NF];
+#pragma unroll
+    for (int a = 0; a < NF; ++a) cn[a] = R(0);
+    build_rhs(cn, b);
     saddle();
     if (cx.t0 + i < cx.Ng - 1) {
       R dinv[B];
@@ -798,7 +740,6 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 #pragma unroll
       for (int r = 0; r < B; ++r) *sc(i, LN::Z0 + r) = b[r];
     }
-    nb_arrive(1 + S + i % S, NT);
   }
   if (act && !ok) atomicExch(flag, 1);
 }
@@ -1025,10 +966,8 @@ struct Nso : NsoBase {
   // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
   // overrides them (tuning runs only).
   int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 64 * 4;
-  int pf_mode = 0;   // SMK_PF (tuning)
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
-    if (const char* e = getenv("SMK_PF")) pf_mode = atoi(e);
     if (const char* e = getenv("SMK_FWD_THRESH")) {
       long long a = 0, b = 0;
       if (sscanf(e, "%lld,%lld", &a, &b) == 2) {
@@ -1129,7 +1068,6 @@ struct Nso : NsoBase {
     c.dt = (R)prm.dt;
     c.ih = (R)(1.0 / L.g.h);
     c.idt = (R)(1.0 / prm.dt);
-    c.pf = pf_mode;
     c.kr = (R)(prm.K / prm.r);
     c.N = prm.n_frames;
     for (int k = 0; k < 3; ++k) c.nf[k] = L.nf[k];
@@ -1161,7 +1099,9 @@ struct Nso : NsoBase {
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     int64_t tot = (int64_t)prm.n_frames * lv[l].nc;
     prof_begin(2, lv[l].nc, st);
-    k_kkt<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(c, r, rhs ? 1 : 0, out); count_launch();
+    if (rhs) k_kkt<DIM, PER, R, true><<<grid_for(tot, 256), 256, 0, st>>>(c, r, out);
+    else k_kkt<DIM, PER, R, false><<<grid_for(tot, 256), 256, 0, st>>>(c, r, out);
+    count_launch();
     prof_end(2, st);
   }
 
@@ -1175,19 +1115,25 @@ struct Nso : NsoBase {
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
   }
 
-  template <int TM, int P>
-  void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, int has_rhs, const int o[3], int mod, const int mm[3],
-                  int64_t M, cudaStream_t st) {
+  template <int TM, int P, bool HR>
+  void launch_fwd_t(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, const int o[3], int mod, const int mm[3], int64_t M,
+                    cudaStream_t st) {
     const size_t shm = (size_t)ring_stages(P) * Line<DIM>::NE * TM * sizeof(R);
-    auto kern = k_scgs_fwd<DIM, PER, R, TM, P>;
+    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
       attr = true;
     }
-    kern<<<(unsigned)((M + TM - 1) / TM), (P + 1) * TM, shm, st>>>(c, r, has_rhs, o[0], o[1], o[2], mod, mm[0], mm[1],
-                                                                   mm[2], scratch, flag);
+    kern<<<(unsigned)((M + TM - 1) / TM), (P + 1) * TM, shm, st>>>(c, r, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                                   scratch, flag);
     count_launch();
+  }
+  template <int TM, int P>
+  void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, bool hr, const int o[3], int mod, const int mm[3],
+                  int64_t M, cudaStream_t st) {
+    if (hr) launch_fwd_t<TM, P, true>(c, r, o, mod, mm, M, st);
+    else launch_fwd_t<TM, P, false>(c, r, o, mod, mm, M, st);
   }
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
@@ -1213,9 +1159,9 @@ struct Nso : NsoBase {
     // colour cells per SM decide the shape: many -> one producer group
     // (throughput), few -> more producer groups per cell (latency)
     int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
-    if (shape == 0) launch_fwd<64, 1>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
-    else if (shape == 1) launch_fwd<32, 2>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
-    else launch_fwd<32, 4>(c, r, rhs ? 1 : 0, o, mod, mm, M, st);
+    if (shape == 0) launch_fwd<64, 1>(c, r, rhs != nullptr, o, mod, mm, M, st);
+    else if (shape == 1) launch_fwd<32, 2>(c, r, rhs != nullptr, o, mod, mm, M, st);
+    else launch_fwd<32, 4>(c, r, rhs != nullptr, o, mod, mm, M, st);
     prof_end(0, st);
     prof_begin(3, M, st);
     {
