@@ -73,6 +73,18 @@ struct Ix {
     c[1] = (int)(o % e1); o /= e1;
     c[0] = (int)o;
   }
+  // 32-bit decodes for per-frame element indices (frame-major launches)
+  __device__ __forceinline__ void face_idx32(int k, int o, int c[3]) const {
+    int e2 = DIM == 3 ? fe(k, 2) : 1, e1 = fe(k, 1);
+    c[2] = o % e2; o /= e2;
+    c[1] = o % e1; o /= e1;
+    c[0] = o;
+  }
+  __device__ __forceinline__ void cell_idx32(int o, int c[3]) const {
+    c[2] = o % n2; o /= n2;
+    c[1] = o % n1; o /= n1;
+    c[0] = o;
+  }
   __device__ __forceinline__ void cell_idx(int64_t o, int c[3]) const {
     c[2] = (int)(o % n2); o /= n2;
     c[1] = (int)(o % n1); o /= n1;
@@ -458,6 +470,16 @@ inline int grid_for(int64_t n, int block) {
   const int64_t cap = 148 * 32;
   return (int)(g < cap ? (g < 1 ? 1 : g) : cap);
 }
+
+// frame-major launch shape: blockIdx.z = frame, blockIdx.y = component (face
+// kernels), a 32-bit grid-stride index over one frame's elements
+inline dim3 frame_grid(int64_t per_frame, int nframes, int block, int comps = 1) {
+  int64_t g = (per_frame + block - 1) / block;
+  if (g > 65535) g = 65535;
+  if (g < 1) g = 1;
+  return dim3((unsigned)g, (unsigned)comps, (unsigned)nframes);
+}
+#define SMK_FRAME_LOOP(e, n) for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < (int)(n); e += gridDim.x * blockDim.x)
 
 #define SMK_GRID_STRIDE(i, n) for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 

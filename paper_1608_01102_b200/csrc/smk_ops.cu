@@ -232,10 +232,11 @@ template <int DIM, bool PER, class R>
 __global__ void k_restrict_cell(Ix<DIM, PER> fx, Ix<DIM, PER> cx, const R* __restrict__ x, R* __restrict__ out,
                                 int N) {
   const int64_t ncc = cx.cells(), ncf = fx.cells();
-  SMK_GRID_STRIDE(t, (int64_t)N * ncc) {
-    int fr = (int)(t / ncc);
+  const int fr = blockIdx.z;
+  SMK_FRAME_LOOP(e, ncc) {
+    const int64_t t = (int64_t)fr * ncc + e;
     int c[3];
-    cx.cell_idx(t - (int64_t)fr * ncc, c);
+    cx.cell_idx32(e, c);
     const R* p = x + (int64_t)fr * ncf;
     R v[2][2];
     int l0 = 2 * c[2];
@@ -271,10 +272,11 @@ template <int DIM, bool PER, class R>
 __global__ void k_prolong_cell(Ix<DIM, PER> cx, Ix<DIM, PER> fx, const R* __restrict__ x, R* __restrict__ out,
                                int N, int accumulate) {
   const int64_t ncc = cx.cells(), ncf = fx.cells();
-  SMK_GRID_STRIDE(t, (int64_t)N * ncf) {
-    int fr = (int)(t / ncf);
+  const int fr = blockIdx.z;
+  SMK_FRAME_LOOP(e, ncf) {
+    const int64_t t = (int64_t)fr * ncf + e;
     int F[3];
-    fx.cell_idx(t - (int64_t)fr * ncf, F);
+    fx.cell_idx32(e, F);
     const R* p = x + (int64_t)fr * ncc;
     int a0, a1, b0, b1, e0 = 0, e1 = 0;
     pro_idx<PER>(F[0], cx.n0, a0, a1);
@@ -303,10 +305,11 @@ template <int DIM, bool PER, class R>
 __global__ void k_restrict_face(Ix<DIM, PER> fx, Ix<DIM, PER> cx, Face3<R> in, FaceW<R> out, int N) {
   const int k = blockIdx.y;
   const int64_t nfc = cx.faces(k), nff = fx.faces(k);
-  SMK_GRID_STRIDE(t, (int64_t)N * nfc) {
-    int fr = (int)(t / nfc);
+  const int fr = blockIdx.z;
+  SMK_FRAME_LOOP(e, nfc) {
+    const int64_t t = (int64_t)fr * nfc + e;
     int c[3];
-    cx.face_idx(k, t - (int64_t)fr * nfc, c);
+    cx.face_idx32(k, e, c);
     const R* p = in.c[k] + (int64_t)fr * nff;
     // candidate fine indices per axis
     int lo[3], cnt[3];
@@ -363,10 +366,11 @@ template <int DIM, bool PER, class R>
 __global__ void k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, Face3<R> in, FaceW<R> out, int N, int accumulate) {
   const int k = blockIdx.y;
   const int64_t nfc = cx.faces(k), nff = fx.faces(k);
-  SMK_GRID_STRIDE(t, (int64_t)N * nff) {
-    int fr = (int)(t / nff);
+  const int fr = blockIdx.z;
+  SMK_FRAME_LOOP(e, nff) {
+    const int64_t t = (int64_t)fr * nff + e;
     int F[3];
-    fx.face_idx(k, t - (int64_t)fr * nff, F);
+    fx.face_idx32(k, e, F);
     const R* p = in.c[k] + (int64_t)fr * nfc;
     int i0[3], i1[3];
     R w0[3], w1[3];
@@ -726,31 +730,27 @@ template <int DIM, bool PER, class R>
 void launch_restrict_cell(const Geo& gf, int N, const R* x, R* out, cudaStream_t st) {
   Geo gc = coarsen(gf);
   Ix<DIM, PER> fx(gf), cx(gc);
-  int64_t n = (int64_t)N * cx.cells();
-  k_restrict_cell<DIM, PER, R><<<grid_for(n, 256), 256, 0, st>>>(fx, cx, x, out, N); count_launch();
+  k_restrict_cell<DIM, PER, R><<<frame_grid(cx.cells(), N, 256), 256, 0, st>>>(fx, cx, x, out, N); count_launch();
 }
 template <int DIM, bool PER, class R>
 void launch_prolong_cell(const Geo& gc, int N, const R* x, R* out, int acc, cudaStream_t st) {
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
-  int64_t n = (int64_t)N * fx.cells();
-  k_prolong_cell<DIM, PER, R><<<grid_for(n, 256), 256, 0, st>>>(cx, fx, x, out, N, acc); count_launch();
+  k_prolong_cell<DIM, PER, R><<<frame_grid(fx.cells(), N, 256), 256, 0, st>>>(cx, fx, x, out, N, acc); count_launch();
 }
 template <int DIM, bool PER, class R>
 void launch_restrict_face(const Geo& gf, int N, Face3<R> in, FaceW<R> out, cudaStream_t st) {
   Geo gc = coarsen(gf);
   Ix<DIM, PER> fx(gf), cx(gc);
-  int64_t n = (int64_t)N * cx.faces(0);
-  dim3 grid(grid_for(n, 256), DIM);
-  k_restrict_face<DIM, PER, R><<<grid, 256, 0, st>>>(fx, cx, in, out, N); count_launch();
+  k_restrict_face<DIM, PER, R><<<frame_grid(cx.faces(0), N, 256, DIM), 256, 0, st>>>(fx, cx, in, out, N);
+  count_launch();
 }
 template <int DIM, bool PER, class R>
 void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int acc, cudaStream_t st) {
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
-  int64_t n = (int64_t)N * fx.faces(0);
-  dim3 grid(grid_for(n, 256), DIM);
-  k_prolong_face<DIM, PER, R><<<grid, 256, 0, st>>>(cx, fx, in, out, N, acc); count_launch();
+  k_prolong_face<DIM, PER, R><<<frame_grid(fx.faces(0), N, 256, DIM), 256, 0, st>>>(cx, fx, in, out, N, acc);
+  count_launch();
 }
 
 #define SMK_INST(DIM, PER, R)                                                                               \

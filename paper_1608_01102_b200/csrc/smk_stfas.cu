@@ -175,10 +175,10 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
-  SMK_GRID_STRIDE(t, (int64_t)cx.N * nc) {
-    const int i = (int)(t / nc);
+  const int i = blockIdx.z;
+  SMK_FRAME_LOOP(e, nc) {
     int c[3];
-    ix.cell_idx(t - (int64_t)i * nc, c);
+    ix.cell_idx32(e, c);
     const Loc<DIM, PER> L(ix, c);
     bool wall[NF];
 #pragma unroll
@@ -849,14 +849,13 @@ __global__ void k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, int N, int o0, int o1, i
   constexpr int NF = 2 * DIM, B = NF + 1;
   const int64_t M = (int64_t)m0 * m1 * m2;
   int64_t nf[3] = {ix.faces(0), ix.faces(1), DIM == 3 ? ix.faces(2) : 0};
-  SMK_GRID_STRIDE(t, (int64_t)N * M) {
-    int i = (int)(t / M);
-    int64_t m = t - (int64_t)i * M;
+  const int i = blockIdx.z;
+  SMK_FRAME_LOOP(m, M) {
     int c[3];
-    int64_t q = m;
-    int q2 = (int)(q % m2); q /= m2;
-    int q1 = (int)(q % m1); q /= m1;
-    c[0] = o0 + mod * (int)q;
+    int q = m;
+    int q2 = q % m2; q /= m2;
+    int q1 = q % m1; q /= m1;
+    c[0] = o0 + mod * q;
     c[1] = o1 + mod * q1;
     c[2] = DIM == 3 ? o2 + mod * q2 : 0;
     const R* xu = xout + (int64_t)(2 * i) * B * M + m;
@@ -965,7 +964,7 @@ struct Nso : NsoBase {
   // forward-kernel shape thresholds (colour cells): >= fwd_big -> TM 64 / P 1,
   // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
   // overrides them (tuning runs only).
-  int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 64 * 4;
+  int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 32 * 2;
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
     if (const char* e = getenv("SMK_FWD_THRESH")) {
@@ -1097,10 +1096,10 @@ struct Nso : NsoBase {
   void residual(int l, const StP<R>& s, const ResP<R>* rhs, const ResP<R>& out, cudaStream_t st) {
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
-    int64_t tot = (int64_t)prm.n_frames * lv[l].nc;
     prof_begin(2, lv[l].nc, st);
-    if (rhs) k_kkt<DIM, PER, R, true><<<grid_for(tot, 256), 256, 0, st>>>(c, r, out);
-    else k_kkt<DIM, PER, R, false><<<grid_for(tot, 256), 256, 0, st>>>(c, r, out);
+    const dim3 grid = frame_grid(lv[l].nc, prm.n_frames, 256);
+    if (rhs) k_kkt<DIM, PER, R, true><<<grid, 256, 0, st>>>(c, r, out);
+    else k_kkt<DIM, PER, R, false><<<grid, 256, 0, st>>>(c, r, out);
     count_launch();
     prof_end(2, st);
   }
@@ -1152,7 +1151,6 @@ struct Nso : NsoBase {
     }
     int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
     if (M == 0) return;
-    int64_t tot = (int64_t)prm.n_frames * M;
     // forward: TM colour cells per CTA (producer + consumer warp per 32);
     // small colours use TM = 32 to spread over all SMs
     prof_begin(0, M, st);
@@ -1172,8 +1170,9 @@ struct Nso : NsoBase {
     }
     prof_end(3, st);
     prof_begin(1, M, st);
-    k_scgs_apply<DIM, PER, R><<<grid_for(tot, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0],
-                                                                   mm[1], mm[2], xout); count_launch();
+    k_scgs_apply<DIM, PER, R><<<frame_grid(M, prm.n_frames, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2],
+                                                                                 mod, mm[0], mm[1], mm[2], xout);
+    count_launch();
     prof_end(1, st);
 
   }
