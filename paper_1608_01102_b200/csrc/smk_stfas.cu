@@ -749,12 +749,22 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 //   L, 1/d of pair i; M_{i+1} recomputed from V), then du, dp of pair i+1
 //   from dv_{i+1}, dv_{i+2}, yu_{i+1} and the same M_{i+1} dv_{i+2}.
 // Writes omega * deltas to xout [2 * pair + (0: u-block, 1: v-block)][entry][m].
-template <int DIM, bool PER, class R>
+// PIPE (small colours, latency-bound): the loads of step i-1 (its stored
+// factors, u-rows and V stencil) are issued before step i computes, so one
+// memory latency overlaps one step instead of adding to it.
+template <int DIM, class R>
+struct BackIn {
+  static constexpr int B = 2 * DIM + 1, NB = NbrSlots<DIM>::NB;
+  R z[B], d[B], l[B * (B - 1) / 2], yu[B];
+  R VC[DIM][NB];
+};
+
+template <int DIM, bool PER, class R, bool PIPE>
 __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
                                                    R* __restrict__ xout) {
   using LN = Line<DIM>;
-  constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB;
+  constexpr int NF = LN::NF, B = LN::B, NL = LN::NL;
   const auto& ix = cx.ix;
   const int N = cx.N;
   const int64_t M = (int64_t)m0 * m1 * m2;
@@ -765,11 +775,30 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   const Loc<DIM, PER> L(ix, cg.c);
   const R idt = cx.idt;
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
-  // t = M_i dv (M_i from the V cache of frame i)
-  auto mdot = [&](int i, const R (&dv)[NF], R (&t)[NF]) {
-    R VC[DIM][NB], Mi[NF][NF];
-    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
-    jac_cached<DIM, R>(cx.c0, idt, VC, cg.wall, Mi);
+  // inputs of step i: factors and z of pair i; u-rows of pair i+1 and the V
+  // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
+  auto fetch = [&](int i, BackIn<DIM, R>& in) {
+    if (i >= 0) {
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        in.z[r] = sc(i, LN::Z0 + r);
+        in.d[r] = sc(i, LN::D0 + r);
+      }
+      if (i + 1 < N) {
+#pragma unroll
+        for (int e = 0; e < NL; ++e) in.l[e] = sc(i, LN::L0 + e);
+      }
+    }
+    if (i + 1 < N) {
+#pragma unroll
+      for (int q = 0; q < B; ++q) in.yu[q] = sc(i + 1, LN::Y0 + q);
+      load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i + 1, cx.nf), in.VC);
+    }
+  };
+  // t = M dv from a V stencil
+  auto mdot = [&](const BackIn<DIM, R>& in, const R (&dv)[NF], R (&t)[NF]) {
+    R Mi[NF][NF];
+    jac_cached<DIM, R>(cx.c0, idt, in.VC, cg.wall, Mi);
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
       R s = R(0);
@@ -778,30 +807,47 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       t[q] = s;
     }
   };
-  // du, dp of pair i from dv_i (dvi), dv_{i+1} and t = M_i dv_{i+1}
-  auto u_delta = [&](int i, const R (&dvi)[NF], const R (&t)[NF]) {
+  // du, dp of pair ip from dv_ip (dvi), yu_ip and t = M_ip dv_{ip+1}
+  auto u_delta = [&](int ip, const R (&yu)[B], const R (&dvi)[NF], const R (&t)[NF]) {
     R a[NF];
     R ga = R(0);
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
-      R s = sc(i, LN::Y0 + q) + dvi[q] * idt - t[q];
+      R s = yu[q] + dvi[q] * idt - t[q];
       a[q] = cg.wall[q] ? R(0) : s;
       ga += cg.gcol[q] * a[q];
     }
-    const R dp = (ga - sc(i, LN::Y0 + NF)) * lc.isig;
-    R* xo = xout + (int64_t)(2 * i) * B * M + m;
+    const R dp = (ga - yu[NF]) * lc.isig;
+    R* xo = xout + (int64_t)(2 * ip) * B * M + m;
 #pragma unroll
     for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
     xo[(int64_t)NF * M] = omega * dp;
   };
   R xn[NF];   // dv of pair i+1
   R t[NF];    // M_{i+1} dv_{i+1}
-  for (int i = N - 1; i >= 0; --i) {
-    R xb[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) xb[r] = sc(i, LN::Z0 + r);
+  for (int q = 0; q < NF; ++q) xn[q] = R(0);
+  BackIn<DIM, R> cur, nxt;
+  if (PIPE) fetch(N - 1, nxt);
+  for (int i = N - 1; i >= -1; --i) {
+    if (PIPE) {
+      cur = nxt;
+      if (i - 1 >= -1) fetch(i - 1, nxt);
+    } else {
+      fetch(i, cur);
+    }
+    R xb[B];
+    if (i + 1 < N) mdot(cur, xn, t);
+    if (i < 0) {
+      R zero[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) zero[q] = R(0);
+      u_delta(0, cur.yu, zero, t);   // dv_0 = 0 (pinned / frozen halo)
+      break;
+    }
+#pragma unroll
+    for (int r = 0; r < B; ++r) xb[r] = cur.z[r];
     if (i + 1 < N) {
-      mdot(i + 1, xn, t);
       R wf[NF], w[B];
 #pragma unroll
       for (int q = 0; q < NF; ++q) wf[q] = t[q];
@@ -813,13 +859,13 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
 #pragma unroll
       for (int r = 1; r < B; ++r)
 #pragma unroll
-        for (int c = 0; c < r; ++c) w[r] -= sc(i, LN::L0 + r * (r - 1) / 2 + c) * w[c];
+        for (int c = 0; c < r; ++c) w[r] -= cur.l[r * (r - 1) / 2 + c] * w[c];
 #pragma unroll
-      for (int r = 0; r < B; ++r) w[r] *= sc(i, LN::D0 + r);
+      for (int r = 0; r < B; ++r) w[r] *= cur.d[r];
 #pragma unroll
       for (int r = B - 2; r >= 0; --r)
 #pragma unroll
-        for (int c = r + 1; c < B; ++c) w[r] -= sc(i, LN::L0 + c * (c - 1) / 2 + r) * w[c];
+        for (int c = r + 1; c < B; ++c) w[r] -= cur.l[c * (c - 1) / 2 + r] * w[c];
 #pragma unroll
       for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
@@ -830,16 +876,11 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       R dvi[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
-      u_delta(i + 1, dvi, t);
+      u_delta(i + 1, cur.yu, dvi, t);
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];
   }
-  R zero[NF];
-#pragma unroll
-  for (int q = 0; q < NF; ++q) zero[q] = R(0);
-  mdot(0, xn, t);
-  u_delta(0, zero, t);   // dv_0 = 0 (pinned / frozen halo)
 }
 
 // x += omega * dx on the colour's unknowns (disjoint across cells)
@@ -965,8 +1006,12 @@ struct Nso : NsoBase {
   // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
   // overrides them (tuning runs only).
   int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 32 * 2;
+  // backward: colours with >= back_flat cells use the unpipelined variant
+  // (occupancy), smaller ones the load-pipelined one.  SMK_BACK_FLAT overrides.
+  int64_t back_flat = 148 * 128 * 4;
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
+    if (const char* e = getenv("SMK_BACK_FLAT")) back_flat = atoll(e);
     if (const char* e = getenv("SMK_FWD_THRESH")) {
       long long a = 0, b = 0;
       if (sscanf(e, "%lld,%lld", &a, &b) == 2) {
@@ -1163,9 +1208,14 @@ struct Nso : NsoBase {
     prof_end(0, st);
     prof_begin(3, M, st);
     {
-      int tpb = M >= 148 * 128 ? 128 : 32;
-      k_scgs_back<DIM, PER, R><<<(unsigned)((M + tpb - 1) / tpb), tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
-                                                                                mm[2], (R)prm.omega, scratch, xout);
+      const int tpb = M >= 148 * 128 ? 128 : 32;
+      const unsigned gb = (unsigned)((M + tpb - 1) / tpb);
+      if (M >= back_flat)
+        k_scgs_back<DIM, PER, R, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                             (R)prm.omega, scratch, xout);
+      else
+        k_scgs_back<DIM, PER, R, true><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                            (R)prm.omega, scratch, xout);
       count_launch();
     }
     prof_end(3, st);

@@ -151,3 +151,78 @@ def test_fp32_bound(nso):
     dev = to_dev(nso, mid, torch.float32)
     nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar)
     assert state_err(dev, want) < 1e-4
+
+
+# Every launch shape of the colour-pass kernels is parity-checked: the bench
+# sizes pick TM 64 / 1 producer group and the unpipelined backward on the fine
+# levels, the tests' small grids would otherwise only reach TM 32 / 4 groups
+# and the pipelined backward.  SMK_FWD_THRESH / SMK_BACK_FLAT are read when a
+# hierarchy (or the one-shot sweep's temporary one) is created.
+SHAPES = {"tm64p1": "0,0", "tm32p2": "1000000000,0", "tm32p4": "1000000000,1000000000"}
+
+
+@pytest.fixture
+def shape_env(monkeypatch):
+    def set_shape(fwd, back_flat):
+        monkeypatch.setenv("SMK_FWD_THRESH", SHAPES[fwd])
+        monkeypatch.setenv("SMK_BACK_FLAT", str(back_flat))
+    return set_shape
+
+
+@pytest.mark.parametrize("fwd", list(SHAPES))
+@pytest.mark.parametrize("back_flat", [0, 1 << 40])
+@pytest.mark.parametrize("dim,bnd", [(2, "neumann"), (3, "neumann"), (3, "periodic")])
+def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back_flat, dim, bnd):
+    shape_env(fwd, back_flat)
+    pb = make_problem(dim, n=8, N=5, boundary=bnd, seed=23)
+    rng = np.random.default_rng(7)
+    st = random_state(pb, rng, 0.05)
+    rhs = random_residual(pb, rng, 0.05)
+    s, cfg = spec_cfg(nso, pb)
+    want = stfas.scgs_smooth(pb, st, rhs)
+    dev = to_dev(nso, st)
+    nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar, rhs=to_dev_res(nso, rhs))
+    assert state_err(dev, want) < 1e-10
+
+
+@pytest.mark.parametrize("fwd", list(SHAPES))
+def test_fp32_sweep_every_kernel_shape(nso, shape_env, fwd):
+    shape_env(fwd, 0)
+    pb = make_problem(3, n=8, N=4, seed=52)
+    s, cfg = spec_cfg(nso, pb)
+    mid = stfas.vcycle(stfas.build_levels(pb, 2), 0, stfas.zero_state(pb.g, pb.N))
+    want = stfas.scgs_smooth(pb, mid)
+    dev = to_dev(nso, mid, torch.float32)
+    nso.scgs_smooth(s, cfg, dev, pb.v0, pb.vstar)
+    assert state_err(dev, want) < 1e-4
+
+
+def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
+    """3D 64^3 x 6 fp64 (32^3 cells per colour -- the bench's fine-level
+    regime): one sweep with every shape; all agree to rounding."""
+    from paper_1608_01102_b200.fields import GridSpec
+    n, N = 64, 6
+    spec = GridSpec(3, (n, n, n), 1.0 / n, "neumann")
+    cfg = nso.StfasConfig(dt=1.0 / N, K=1e3, r=1e3, omega=0.8, color_mod=2)
+    g = torch.Generator().manual_seed(5)
+    shp = lambda k: (N,) + tuple(n + (a == k) for a in range(3))
+    V = tuple((0.1 * torch.randn(shp(k), generator=g, dtype=torch.float64)) for k in range(3))
+    U = tuple((0.1 * torch.randn(shp(k), generator=g, dtype=torch.float64)) for k in range(3))
+    PB = 0.1 * torch.randn((N, n, n, n), generator=g, dtype=torch.float64)
+    P = 0.1 * torch.randn((N, n, n, n), generator=g, dtype=torch.float64)
+    vs = tuple((0.1 * torch.randn(shp(k), generator=g, dtype=torch.float64)) for k in range(3))
+    v0 = tuple(torch.zeros(shp(k)[1:], dtype=torch.float64) for k in range(3))
+    outs = []
+    for fwd, bf in [("tm64p1", 0), ("tm32p2", 1 << 40), ("tm32p4", 1 << 40)]:
+        shape_env(fwd, bf)
+        dev = nso.SpacetimeState.from_arrays([c.numpy() for c in V], PB.numpy(), [c.numpy() for c in U],
+                                             P.numpy(), dtype=torch.float64)
+        nso.scgs_smooth(spec, cfg, dev, [c.numpy() for c in v0], [c.numpy() for c in vs])
+        outs.append(dev.numpy())
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            if isinstance(a, (tuple, list)):
+                for x, y in zip(a, b):
+                    assert rel_err(x, y) < 1e-12
+            else:
+                assert rel_err(a, b) < 1e-12
