@@ -422,6 +422,26 @@ __device__ __forceinline__ R JT_at(const Ix<DIM, PER>& ix, R c0, int k, const in
   return Tadj_at<DIM, PER, R>(ix, c0, k, g, v, u) - S_at<DIM, PER, R>(ix, c0, k, g, v, u);
 }
 
+// ---------------------------------------------------------------------------
+// Paired arithmetic for the dense per-cell block algebra: fp32 maps to the
+// sm_100 packed FFMA2 / FMUL2 (two independent fused multiply-adds per
+// instruction, each rounded exactly like the scalar FFMA), fp64 to two DFMAs.
+// `a` is broadcast to both lanes.
+// ---------------------------------------------------------------------------
+template <class R> struct PairOf;
+template <> struct PairOf<float> { using T = float2; };
+template <> struct PairOf<double> { using T = double2; };
+template <class R> using R2 = typename PairOf<R>::T;
+
+__device__ __forceinline__ float2 p2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 p2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 fma2s(float a, float2 b, float2 c) { return __ffma2_rn(make_float2(a, a), b, c); }
+__device__ __forceinline__ double2 fma2s(double a, double2 b, double2 c) {
+  return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
+}
+__device__ __forceinline__ float2 mul2s(float a, float2 b) { return __fmul2_rn(make_float2(a, a), b); }
+__device__ __forceinline__ double2 mul2s(double a, double2 b) { return make_double2(a * b.x, a * b.y); }
+
 // explicit-width |x| (an unqualified abs() on a float can bind to int abs)
 __device__ __forceinline__ float rabs(float x) { return fabsf(x); }
 __device__ __forceinline__ double rabs(double x) { return fabs(x); }

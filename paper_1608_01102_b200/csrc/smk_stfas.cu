@@ -268,6 +268,16 @@ __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) 
   return ok;
 }
 
+// 1/x for the pivots: fp32 uses the hardware approximation plus one Newton
+// step (<= 1 ulp for the normal, well-scaled pivots of these blocks; no IEEE
+// slow-path call sites in the consumer loop), fp64 the IEEE division.
+__device__ __forceinline__ float pivot_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * (2.0f - x * r);
+}
+__device__ __forceinline__ double pivot_rcp(double x) { return 1.0 / x; }
+
 // In-place LDL^T of a symmetric B x B matrix held in the lower triangle of T
 // (natural order, no pivoting -- used for the saddle blocks whose faces part
 // is positive definite): on exit T[r][c] (c < r) = L[r][c], dinv = 1 / d.
@@ -278,7 +288,7 @@ __device__ __forceinline__ bool ldlt(R (&T)[B][B], R (&dinv)[B], R tiny) {
   for (int col = 0; col < B; ++col) {
     const R piv = T[col][col];
     if (!(rabs(piv) > tiny)) ok = false;
-    dinv[col] = R(1) / piv;
+    dinv[col] = pivot_rcp(piv);
     R l[B];
 #pragma unroll
     for (int r = col + 1; r < B; ++r) l[r] = T[r][col] * dinv[col];
@@ -584,22 +594,36 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
   // D faces block of pair ip: (PM)^T PM + [ip+1<N] P/dt^2 + alpha / wall identity
   // (lower triangle)
-  auto diag_block = [&](int ip, const R (&PM)[NF][NF], R (&T)[B][B]) {
+  const R idt2 = idt * idt;
+  R gs[NF];   // g * idt^2 / sigma: P idt^2 = idt^2 I - g gs^T on the unknown faces
+#pragma unroll
+  for (int q = 0; q < NF; ++q) gs[q] = cg.gcol[q] * lc.isig * idt2;
+  // The dense block algebra below runs on lane pairs (columns 2h, 2h+1):
+  // FFMA2 with a broadcast scalar in fp32, each lane rounded exactly like the
+  // scalar FFMA of the same expression (same operand order, same summation
+  // order), so the pairing does not change the results.
+  constexpr int NH = NF / 2;
+  using P2 = R2<R>;
+  auto lo_hi = [](const P2& v, int e) -> R { return e ? v.y : v.x; };
+  auto diag_block = [&](int ip, const P2 (&PM)[NF][NH], R (&T)[B][B]) {
     const bool nx = ip + 1 < N;
     const R alpha = (cx.t0 + ip < cx.Ng - 1) ? cx.kr : R(0);
 #pragma unroll
     for (int a = 0; a < NF; ++a)
 #pragma unroll
-      for (int b = 0; b <= a; ++b) {
-        R s = R(0);
+      for (int h = 0; h <= (a >> 1); ++h) {
+        P2 acc = p2(R(0), R(0));
 #pragma unroll
-        for (int t = 0; t < NF; ++t) s += PM[t][a] * PM[t][b];
-        if (nx) {
-          R pab = (a == b && !cg.wall[a] ? R(1) : R(0)) - cg.gcol[a] * cg.gcol[b] * lc.isig;
-          s += pab * idt * idt;
+        for (int t = 0; t < NF; ++t) acc = fma2s(lo_hi(PM[t][a >> 1], a & 1), PM[t][h], acc);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int b = 2 * h + e;
+          if (b > a) continue;
+          R s = lo_hi(acc, e);
+          if (nx) s -= cg.gcol[a] * gs[b];
+          if (a == b) s += cg.wall[a] ? R(1) : alpha + (nx ? idt2 : R(0));
+          T[a][b] = s;
         }
-        if (a == b) s += cg.wall[a] ? R(1) : alpha;
-        T[a][b] = s;
       }
   };
   // c = P yu + g yu_p / sigma of pair i (from the ring)
@@ -613,7 +637,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   };
   // M_i from the V stencil, then P M_i, the partial rhs yv + M^T c and the
   // dpbar-row rhs of pair i
-  auto mats_of = [&](int i, const R (&cv)[NF], R (&PM)[NF][NF], R (&xrr)[NF], R& yc) {
+  auto mats_of = [&](int i, const R (&cv)[NF], P2 (&PM)[NF][NH], R (&xrr)[NF], R& yc) {
     R VC[DIM][NB];
 #pragma unroll
     for (int a = 0; a < DIM; ++a)
@@ -621,22 +645,29 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
       for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(i, LN::E_VS + a * NB + sl);
     R Mx[NF][NF];
     jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
+    P2 Mp[NF][NH];
 #pragma unroll
-    for (int a = 0; a < NF; ++a) {
-      R s = *slot(i, LN::E_YV + a);
+    for (int t = 0; t < NF; ++t)
 #pragma unroll
-      for (int t = 0; t < NF; ++t) s += Mx[t][a] * cv[t];
-      xrr[a] = s;
+      for (int h = 0; h < NH; ++h) Mp[t][h] = p2(Mx[t][2 * h], Mx[t][2 * h + 1]);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      P2 s2 = p2(*slot(i, LN::E_YV + 2 * h), *slot(i, LN::E_YV + 2 * h + 1));
+#pragma unroll
+      for (int t = 0; t < NF; ++t) s2 = fma2s(cv[t], Mp[t][h], s2);
+      xrr[2 * h] = s2.x;
+      xrr[2 * h + 1] = s2.y;
     }
     yc = *slot(i, LN::E_YV + NF);
+    // P M column pairs: d = isig g^T M, PM = M - g d on the unknown rows
 #pragma unroll
-    for (int b = 0; b < NF; ++b) {
-      R col[NF];
+    for (int h = 0; h < NH; ++h) {
+      P2 d = p2(R(0), R(0));
 #pragma unroll
-      for (int a = 0; a < NF; ++a) col[a] = Mx[a][b];
-      lc.projP(col);
+      for (int q = 0; q < NF; ++q) d = fma2s(cg.gcol[q], Mp[q][h], d);
+      d = mul2s(lc.isig, d);
 #pragma unroll
-      for (int a = 0; a < NF; ++a) PM[a][b] = col[a];
+      for (int a = 0; a < NF; ++a) PM[a][h] = cg.wall[a] ? p2(R(0), R(0)) : fma2s(-cg.gcol[a], d, Mp[a][h]);
     }
   };
   R T[B][B];      // lower triangle: D~ of the current pair, then its L
@@ -646,7 +677,8 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   bool ok = true;
   nb_sync(1 + 0, NT);
   {
-    R PM[NF][NF], cv[NF];
+    P2 PM[NF][NH];
+    R cv[NF];
     c_of(0, cv);
     mats_of(0, cv, PM, xr, ycell);
     diag_block(0, PM, T);
@@ -687,38 +719,45 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         *sc(i, LN::Z0 + r) = b[r];
       }
     }
-    R PM[NF][NF];
+    P2 PM[NF][NH];
     mats_of(i + 1, cn, PM, xr, ycell);
 #pragma unroll
-    for (int a = 0; a < NF; ++a) {
-      R s = R(0);
+    for (int h = 0; h < NH; ++h) {
+      P2 s2 = p2(R(0), R(0));
 #pragma unroll
-      for (int t = 0; t < NF; ++t) s += PM[t][a] * b[t];
-      sz[a] = s;
+      for (int t = 0; t < NF; ++t) s2 = fma2s(b[t], PM[t][h], s2);
+      sz[2 * h] = s2.x;
+      sz[2 * h + 1] = s2.y;
     }
-    // Y = L^-1 [PM; 0], column by column (row NF starts at 0)
-    R Y[B][NF];
+    // Y = L^-1 [PM; 0] on column pairs (row NF starts at 0)
+    P2 Y[B][NH];
 #pragma unroll
-    for (int j = 0; j < NF; ++j) {
+    for (int r = 0; r < B; ++r)
 #pragma unroll
-      for (int r = 0; r < B; ++r) {
-        R s = r < NF ? PM[r][j] : R(0);
+      for (int h = 0; h < NH; ++h) {
+        P2 s2 = r < NF ? PM[r][h] : p2(R(0), R(0));
 #pragma unroll
-        for (int c = 0; c < r; ++c) s -= T[r][c] * Y[c][j];
-        Y[r][j] = s;
+        for (int c = 0; c < r; ++c) s2 = fma2s(-T[r][c], Y[c][h], s2);
+        Y[r][h] = s2;
       }
-    }
     diag_block(i + 1, PM, T);
     // Schur complement of the eliminated pair: - Y^T diag(1/d) Y / dt^2
 #pragma unroll
-    for (int a = 0; a < NF; ++a)
+    for (int k = 0; k < B; ++k) dinv[k] *= idt2;
 #pragma unroll
-      for (int c = 0; c <= a; ++c) {
-        R s = R(0);
+    for (int a = 0; a < NF; ++a) {
+      R DY[B];
 #pragma unroll
-        for (int k = 0; k < B; ++k) s += Y[k][a] * dinv[k] * Y[k][c];
-        T[a][c] -= s * idt * idt;
+      for (int k = 0; k < B; ++k) DY[k] = lo_hi(Y[k][a >> 1], a & 1) * dinv[k];
+#pragma unroll
+      for (int h = 0; h <= (a >> 1); ++h) {
+        P2 s2 = p2(R(0), R(0));
+#pragma unroll
+        for (int k = 0; k < B; ++k) s2 = fma2s(DY[k], Y[k][h], s2);
+        T[a][2 * h] -= s2.x;
+        if (2 * h + 1 <= a) T[a][2 * h + 1] -= s2.y;
       }
+    }
   }
   {
     // last pair: no coupling to a next pair; only z is needed
