@@ -210,8 +210,12 @@ struct NbrField {
 // face frame is 2.1M elements); the frame base pointer carries the rest.
 // Periodic: wrapped through Ix (cold path, not used by the benchmarks).
 // ---------------------------------------------------------------------------
-template <int DIM, bool PER>
+// NX > 0: the grid is a compile-time NX^3 Neumann cube, so every stencil
+// offset below is an immediate (LDG [R + imm]) and only the cell's own face
+// offsets are runtime values.
+template <int DIM, bool PER, int NX = 0>
 struct Loc {
+  static_assert(NX == 0 || (DIM == 3 && !PER), "compile-time extents: 3D Neumann cubes only");
   int c[3];
   bool lo[3], hi[3];
   int of[2 * DIM];   // offsets of the cell's own faces (q = 2k + side)
@@ -237,11 +241,13 @@ struct Loc {
   // stride of face component k along axis a (axis 2 / the 2D last axis: 1)
   __device__ __forceinline__ static int fstride(const Ix<DIM, PER>& ix, int k, int a) {
     if (a == 2) return 1;
+    if (NX > 0) return a == 0 ? (NX + (k == 1)) * (NX + (k == 2)) : NX + (k == 2);
     if (DIM == 2) return a == 0 ? ix.fe(k, 1) : 1;
     return a == 0 ? ix.fe(k, 1) * ix.fe(k, 2) : ix.fe(k, 2);
   }
   __device__ __forceinline__ static int cstride(const Ix<DIM, PER>& ix, int a) {
     if (a == 2) return 1;
+    if (NX > 0) return a == 0 ? NX * NX : NX;
     if (DIM == 2) return a == 0 ? ix.n1 : 1;
     return a == 0 ? ix.n1 * ix.n2 : ix.n2;
   }
@@ -267,8 +273,8 @@ struct Loc {
 
 // register cache of one face field around a cell (NbrSlots layout), loaded
 // through Loc; slots a stencil does not use are dead and never loaded
-template <int DIM, bool PER, class R>
-__device__ __forceinline__ void load_nbr(const Ix<DIM, PER>& ix, const Loc<DIM, PER>& L, const Face3<R>& f,
+template <int DIM, bool PER, class R, class LocT>
+__device__ __forceinline__ void load_nbr(const Ix<DIM, PER>& ix, const LocT& L, const Face3<R>& f,
                                          R (&val)[DIM][NbrSlots<DIM>::NB]) {
 #pragma unroll
   for (int a = 0; a < DIM; ++a)

@@ -83,8 +83,8 @@ struct KktCtx {
 // (the smoother assembles only unknown rows).  Same term order as
 // oracle/stfas.py kkt_residual; 1/h and 1/dt are multiplied, not divided.
 // ---------------------------------------------------------------------------
-template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS, bool HR>
-__device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const Loc<DIM, PER>& L,
+template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS, bool HR, class LocT>
+__device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const LocT& L,
                                           const bool (&wall)[2 * DIM], int i,
                                           const R (&VC)[DIM][NbrSlots<DIM>::NB],
                                           const R (&UC)[DIM][NbrSlots<DIM>::NB], const R (&vp)[2 * DIM],
@@ -170,7 +170,7 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
 // upper wall face of the last cell along each axis (0 - rhs).  Neighbour
 // values come from the register caches (every V / U value the cell's faces
 // need is read once per thread, through L1).
-template <int DIM, bool PER, class R, bool HR>
+template <int DIM, bool PER, class R, bool HR, int NX>
 __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out) {
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
   SMK_FRAME_LOOP(e, nc) {
     int c[3];
     ix.cell_idx32(e, c);
-    const Loc<DIM, PER> L(ix, c);
+    const Loc<DIM, PER, NX> L(ix, c);
     bool wall[NF];
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
@@ -514,7 +514,7 @@ __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
                                                                    : 1;
 }
 
-template <int DIM, bool PER, class R, int TM, int P, bool HR>
+template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX>
 __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R)))
     k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int o0, int o1, int o2, int mod, int m0, int m1,
                int m2, R* __restrict__ scratch, int* flag) {
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   auto slot = [&](int i, int e) -> R* { return ring + ((i % S) * NE + e) * TM + lane; };
 
   if (producer) {
-    const Loc<DIM, PER> L(ix, cg.c);
+    const Loc<DIM, PER, NX> L(ix, cg.c);
     R vp[NF];   // V_{i-1} at the own faces (carried when one group builds every pair)
     if (P == 1) {
 #pragma unroll
@@ -798,7 +798,7 @@ struct BackIn {
   R VC[DIM][NB];
 };
 
-template <int DIM, bool PER, class R, bool PIPE>
+template <int DIM, bool PER, class R, bool PIPE, int NX>
 __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
                                                    R* __restrict__ xout) {
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   if (m >= M) return;
   const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
   const auto& cg = lc.cg;
-  const Loc<DIM, PER> L(ix, cg.c);
+  const Loc<DIM, PER, NX> L(ix, cg.c);
   const R idt = cx.idt;
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
   // inputs of step i: factors and z of pair i; u-rows of pair i+1 and the V
@@ -1182,8 +1182,11 @@ struct Nso : NsoBase {
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     prof_begin(2, lv[l].nc, st);
     const dim3 grid = frame_grid(lv[l].nc, prm.n_frames, 256);
-    if (rhs) k_kkt<DIM, PER, R, true><<<grid, 256, 0, st>>>(c, r, out);
-    else k_kkt<DIM, PER, R, false><<<grid, 256, 0, st>>>(c, r, out);
+    with_nx(l, [&](auto nxc) {
+      constexpr int NXv = decltype(nxc)::value;
+      if (rhs) k_kkt<DIM, PER, R, true, NXv><<<grid, 256, 0, st>>>(c, r, out);
+      else k_kkt<DIM, PER, R, false, NXv><<<grid, 256, 0, st>>>(c, r, out);
+    });
     count_launch();
     prof_end(2, st);
   }
@@ -1198,11 +1201,28 @@ struct Nso : NsoBase {
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
   }
 
-  template <int TM, int P, bool HR>
+  // compile-time cube extent of level l for the big-colour kernels (0 = runtime)
+  int cube_nx(int l) const {
+    if (DIM != 3 || PER) return 0;
+    const Geo& g = lv[l].g;
+    if (g.n[0] != g.n[1] || g.n[1] != g.n[2]) return 0;
+    return (g.n[0] == 64 || g.n[0] == 128) ? g.n[0] : 0;
+  }
+  template <class F>
+  void with_nx(int l, F&& f) {
+    if constexpr (DIM == 3 && !PER) {
+      const int nx = cube_nx(l);
+      if (nx == 128) return f(std::integral_constant<int, 128>{});
+      if (nx == 64) return f(std::integral_constant<int, 64>{});
+    }
+    f(std::integral_constant<int, 0>{});
+  }
+
+  template <int TM, int P, bool HR, int NX>
   void launch_fwd_t(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, const int o[3], int mod, const int mm[3], int64_t M,
                     cudaStream_t st) {
     const size_t shm = (size_t)ring_stages(P) * Line<DIM>::NE * TM * sizeof(R);
-    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR>;
+    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -1212,11 +1232,11 @@ struct Nso : NsoBase {
                                                                    scratch, flag);
     count_launch();
   }
-  template <int TM, int P>
+  template <int TM, int P, int NX>
   void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, bool hr, const int o[3], int mod, const int mm[3],
                   int64_t M, cudaStream_t st) {
-    if (hr) launch_fwd_t<TM, P, true>(c, r, o, mod, mm, M, st);
-    else launch_fwd_t<TM, P, false>(c, r, o, mod, mm, M, st);
+    if (hr) launch_fwd_t<TM, P, true, NX>(c, r, o, mod, mm, M, st);
+    else launch_fwd_t<TM, P, false, NX>(c, r, o, mod, mm, M, st);
   }
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
@@ -1241,20 +1261,30 @@ struct Nso : NsoBase {
     // colour cells per SM decide the shape: many -> one producer group
     // (throughput), few -> more producer groups per cell (latency)
     int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
-    if (shape == 0) launch_fwd<64, 1>(c, r, rhs != nullptr, o, mod, mm, M, st);
-    else if (shape == 1) launch_fwd<32, 2>(c, r, rhs != nullptr, o, mod, mm, M, st);
-    else launch_fwd<32, 4>(c, r, rhs != nullptr, o, mod, mm, M, st);
+    if (shape == 2) {
+      launch_fwd<32, 4, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
+    } else {
+      with_nx(l, [&](auto nxc) {
+        constexpr int NXv = decltype(nxc)::value;
+        if (shape == 0) launch_fwd<64, 1, NXv>(c, r, rhs != nullptr, o, mod, mm, M, st);
+        else launch_fwd<32, 2, NXv>(c, r, rhs != nullptr, o, mod, mm, M, st);
+      });
+    }
     prof_end(0, st);
     prof_begin(3, M, st);
     {
       const int tpb = M >= 148 * 128 ? 128 : 32;
       const unsigned gb = (unsigned)((M + tpb - 1) / tpb);
-      if (M >= back_flat)
-        k_scgs_back<DIM, PER, R, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+      if (M >= back_flat) {
+        with_nx(l, [&](auto nxc) {
+          constexpr int NXv = decltype(nxc)::value;
+          k_scgs_back<DIM, PER, R, false, NXv><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                                  (R)prm.omega, scratch, xout);
+        });
+      } else {
+        k_scgs_back<DIM, PER, R, true, 0><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
                                                              (R)prm.omega, scratch, xout);
-      else
-        k_scgs_back<DIM, PER, R, true><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                            (R)prm.omega, scratch, xout);
+      }
       count_launch();
     }
     prof_end(3, st);
