@@ -55,6 +55,19 @@ def vcycle_values_per_cts(dim, levels):
     return tot
 
 
+def traffic_ref(workload, kernel):
+    """Measured DRAM bytes per level-0 launch of `kernel` for `workload` from
+    the committed ncu capture summary (profiles/traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d[workload][kernel]
+        return {"bytes_per_launch": float(e["bytes_per_launch"]), "source": e["source"]}
+    except Exception:
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -257,6 +270,8 @@ def main():
         dist.barrier()
     clk = clocks.stop() if clocks else None
     kprof = {name: hier.profile_read(kind) for kind, name in hier.KERNELS.items()}
+    kprof_lv = {name: [hier.profile_read(kind, level=l) for l in range(hier.levels)]
+                for kind, name in hier.KERNELS.items()}
     hier.profile(False)
     ms = t_total / args.steps
     if world > 1:
@@ -268,19 +283,26 @@ def main():
         ri, r2 = slab.norms([state])
     else:
         ri, r2 = hier.residual_norms(state)
-    value = w.cell_timesteps / (ms / 1000.0)
+    value = w.cell_timesteps / (ms / 1000.0)   # strong scaling: the whole volume per V-cycle
     hbm, peak_kind = peaks()
     esz = 4 if w.dtype == torch.float32 else 8
-    # dominant kernel = the colour-pass forward kernel k_scgs_fwd; its
-    # algorithmic bytes are the sweep traffic of the cells it updates
-    # (SURVEY §8d): (2s + g) values per colour cell-timestep
+    # dominant kernel: the fine-level forward elimination k_scgs_fwd (level 0).
+    # Algorithmic bytes per launch = SURVEY §8d's smoother figure for the cells
+    # the launch updates: (2s + g) values per colour cell-timestep (read and
+    # write the state, read the guide; level 0 has no rhs) x colour cells x
+    # frames.  traffic = measured DRAM bytes per L0 launch from the committed
+    # ncu capture of this workload (profiles/traffic.json), or null.
     kname = "k_scgs_fwd"
-    k_ms, k_n, k_cells = kprof[kname]
-    k_bytes = k_cells * sweep_values(w.dim) * esz
+    k_ms, k_n, k_cells = kprof_lv[kname][0]
     k_avg_ms = k_ms / max(k_n, 1)
-    k_achieved = (k_bytes / max(k_n, 1)) / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
-    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
-                   "share_of_step": (v[0] / args.steps) / ms if ms else None} for k, v in kprof.items()}
+    k_bytes_launch = (k_cells / max(k_n, 1)) * sweep_values(w.dim) * esz
+    k_achieved = k_bytes_launch / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
+    traffic = traffic_ref(w.name, kname)
+    kernels = {}
+    for k, v in kprof.items():
+        kernels[k] = {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                      "share_of_step": (v[0] / args.steps) / ms if ms else None,
+                      "ms_per_step_by_level": [round(x[0] / args.steps, 3) for x in kprof_lv[k]]}
     vc_bytes = vcycle_values_per_cts(w.dim, hier.levels) * esz * w.cell_timesteps
     vc_gbs = vc_bytes / (ms / 1000.0) / 1e9 / world
 
@@ -337,11 +359,16 @@ def main():
                        "parallelism": f"time-slabs x{world}" if world > 1 else "single",
                        "l2": "flushed" if flush is not None else "inputs larger than L2",
                        "residual_inf_after": ri},
-            "roofline": {"bound": "hbm", "kernel": kname, "achieved": k_achieved, "peak": hbm,
+            "roofline": {"bound": "hbm", "kernel": f"{kname} (level 0)", "achieved": k_achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": k_achieved / hbm,
-                         "traffic": None, "avg_launch_ms": k_avg_ms, "launches": k_n,
-                         "share_of_step": (k_ms / args.steps) / ms if ms else None},
-            "smoother_kernels": kernels,
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_gbs": (traffic["bytes_per_launch"] / (k_avg_ms / 1000.0) / 1e9) if traffic else None,
+                         "traffic_frac": (traffic["bytes_per_launch"] / (k_avg_ms / 1000.0) / 1e9 / hbm)
+                         if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "algorithmic_bytes_per_launch": k_bytes_launch, "avg_launch_ms": k_avg_ms,
+                         "launches": k_n, "share_of_step": (k_ms / args.steps) / ms if ms else None},
+            "kernels": kernels,
             "vcycle_hbm": {"achieved_per_gpu": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
                            "algorithmic_bytes": vc_bytes},
             "e2e": e2e,

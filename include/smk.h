@@ -185,12 +185,17 @@ int smk_nso_set_guide(smk_nso* h, const void* const v0[], const void* const vsta
 int smk_nso_vcycle(smk_nso* h, const smk_state* s, void* stream);
 /* ||f||_inf and ||f||_2 of the top level (synchronising). */
 int smk_nso_residual_norms(smk_nso* h, const smk_state* s, double* res_inf, double* res_l2, void* stream);
-/* Bracket every smoother kernel launch with CUDA events on the launching
- * stream (enable != 0 also resets the record).  profile_read returns, for
- * kernel kind 0 (assemble), 1 (time-line solve) or 2 (apply), the summed
- * kernel time, the launch count and the cell-timesteps processed. */
+/* Bracket every colour-pass and residual kernel launch with CUDA events on
+ * the launching stream (enable != 0 also resets the record).  profile_read
+ * returns, for kernel kind 0 (k_scgs_fwd, forward elimination), 1
+ * (k_scgs_apply), 2 (k_kkt, residual) or 3 (k_scgs_back, back substitution),
+ * the summed kernel time, the launch count and the cell-timesteps processed
+ * (colour cells x frames; all cells x frames for the residual), over all
+ * levels; profile_read_level restricts it to one hierarchy level. */
 int smk_nso_profile(smk_nso* h, int enable);
 int smk_nso_profile_read(smk_nso* h, int kind, double* ms, long long* launches, long long* cell_timesteps);
+int smk_nso_profile_read_level(smk_nso* h, int kind, int level, double* ms, long long* launches,
+                               long long* cell_timesteps);
 /* Subtract per-frame means of p and pbar (gauge). */
 int smk_nso_gauge_fix(smk_nso* h, const smk_state* s, void* stream);
 /* solve_nso: V-cycles until ||f||_inf <= eps (or

@@ -990,7 +990,7 @@ struct NsoBase {
                                const void* const unext[], const void* const vs[], const smk_residual* rhs,
                                cudaStream_t st) = 0;
   virtual int profile(int enable) = 0;
-  virtual int profile_read(int kind, double* ms, long long* launches, long long* cells) = 0;
+  virtual int profile_read(int kind, int level, double* ms, long long* launches, long long* cells) = 0;
   virtual int64_t bytes() const = 0;
 };
 
@@ -1009,27 +1009,34 @@ struct Nso : NsoBase {
   const void* top_v0[3] = {nullptr, nullptr, nullptr};
   const void* top_vs[3] = {nullptr, nullptr, nullptr};
   bool guide_set = false;
-  // optional CUDA-event profile of the smoother's colour kernel
+  // optional CUDA-event profile of the kernels of each colour pass / residual,
+  // per kind and level
   bool prof = false;
   static constexpr int NKIND = 4;  // 0 forward, 1 apply, 2 residual, 3 backward
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[NKIND];
+  struct Ev {
+    cudaEvent_t a, b;
+    int level;
+    int64_t cells;
+  };
+  std::vector<Ev> ev[NKIND];
   size_t ev_used[NKIND] = {0, 0, 0, 0};
-  int64_t prof_cells[NKIND] = {0, 0, 0, 0};  // cell-timesteps processed
 
-  void prof_begin(int kind, int64_t M, cudaStream_t st) {
+  void prof_begin(int kind, int level, int64_t M, cudaStream_t st) {
     if (!prof) return;
     if (ev_used[kind] == ev[kind].size()) {
-      cudaEvent_t a, b;
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
-      ev[kind].push_back({a, b});
+      Ev e{};
+      cudaEventCreate(&e.a);
+      cudaEventCreate(&e.b);
+      ev[kind].push_back(e);
     }
-    prof_cells[kind] += M * prm.n_frames;
-    cudaEventRecord(ev[kind][ev_used[kind]].first, st);
+    Ev& e = ev[kind][ev_used[kind]];
+    e.level = level;
+    e.cells = M * prm.n_frames;
+    cudaEventRecord(e.a, st);
   }
   void prof_end(int kind, cudaStream_t st) {
     if (!prof) return;
-    cudaEventRecord(ev[kind][ev_used[kind]].second, st);
+    cudaEventRecord(ev[kind][ev_used[kind]].b, st);
     ++ev_used[kind];
   }
 
@@ -1105,31 +1112,33 @@ struct Nso : NsoBase {
   int levels() const override { return (int)lv.size(); }
   int profile(int enable) override {
     prof = enable != 0;
-    for (int k = 0; k < NKIND; ++k) {
-      ev_used[k] = 0;
-      prof_cells[k] = 0;
-    }
+    for (int k = 0; k < NKIND; ++k) ev_used[k] = 0;
     return SMK_OK;
   }
-  int profile_read(int kind, double* ms, long long* launches, long long* cells) override {
+  int profile_read(int kind, int level, double* ms, long long* launches, long long* cells) override {
     if (kind < 0 || kind >= NKIND) { set_error("bad profile kind"); return SMK_ERR_ARG; }
     double tot = 0.0;
+    long long n = 0, c = 0;
     for (size_t i = 0; i < ev_used[kind]; ++i) {
-      cudaEventSynchronize(ev[kind][i].second);
+      const Ev& e = ev[kind][i];
+      if (level >= 0 && e.level != level) continue;
+      cudaEventSynchronize(e.b);
       float t = 0.f;
-      cudaEventElapsedTime(&t, ev[kind][i].first, ev[kind][i].second);
+      cudaEventElapsedTime(&t, e.a, e.b);
       tot += t;
+      ++n;
+      c += e.cells;
     }
     if (ms) *ms = tot;
-    if (launches) *launches = (long long)ev_used[kind];
-    if (cells) *cells = (long long)prof_cells[kind];
+    if (launches) *launches = n;
+    if (cells) *cells = c;
     return cuda_check("nso_profile_read");
   }
   ~Nso() override {
     for (int k = 0; k < NKIND; ++k)
       for (auto& e : ev[k]) {
-        cudaEventDestroy(e.first);
-        cudaEventDestroy(e.second);
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
       }
   }
   int64_t bytes() const override { return nbytes; }
@@ -1180,7 +1189,7 @@ struct Nso : NsoBase {
   void residual(int l, const StP<R>& s, const ResP<R>* rhs, const ResP<R>& out, cudaStream_t st) {
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
-    prof_begin(2, lv[l].nc, st);
+    prof_begin(2, l, lv[l].nc, st);
     const dim3 grid = frame_grid(lv[l].nc, prm.n_frames, 256);
     with_nx(l, [&](auto nxc) {
       constexpr int NXv = decltype(nxc)::value;
@@ -1257,7 +1266,7 @@ struct Nso : NsoBase {
     if (M == 0) return;
     // forward: TM colour cells per CTA (producer + consumer warp per 32);
     // small colours use TM = 32 to spread over all SMs
-    prof_begin(0, M, st);
+    prof_begin(0, l, M, st);
     // colour cells per SM decide the shape: many -> one producer group
     // (throughput), few -> more producer groups per cell (latency)
     int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
@@ -1271,7 +1280,7 @@ struct Nso : NsoBase {
       });
     }
     prof_end(0, st);
-    prof_begin(3, M, st);
+    prof_begin(3, l, M, st);
     {
       const int tpb = M >= 148 * 128 ? 128 : 32;
       const unsigned gb = (unsigned)((M + tpb - 1) / tpb);
@@ -1288,7 +1297,7 @@ struct Nso : NsoBase {
       count_launch();
     }
     prof_end(3, st);
-    prof_begin(1, M, st);
+    prof_begin(1, l, M, st);
     k_scgs_apply<DIM, PER, R><<<frame_grid(M, prm.n_frames, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2],
                                                                                  mod, mm[0], mm[1], mm[2], xout);
     count_launch();
@@ -1613,7 +1622,12 @@ int smk_nso_profile(smk_nso* h, int enable) {
 
 int smk_nso_profile_read(smk_nso* h, int kind, double* ms, long long* launches, long long* cells) {
   if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
-  return h->impl->profile_read(kind, ms, launches, cells);
+  return h->impl->profile_read(kind, -1, ms, launches, cells);
+}
+
+int smk_nso_profile_read_level(smk_nso* h, int kind, int level, double* ms, long long* launches, long long* cells) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->profile_read(kind, level, ms, launches, cells);
 }
 int64_t smk_nso_device_bytes(const smk_nso* h) { return h ? h->impl->bytes() : 0; }
 

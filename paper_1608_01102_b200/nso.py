@@ -246,11 +246,16 @@ class StfasHierarchy:
 
     KERNELS = {0: "k_scgs_fwd", 1: "k_scgs_apply", 2: "k_kkt", 3: "k_scgs_back"}
 
-    def profile_read(self, kind=0):
-        """(summed kernel ms, launches, cell-timesteps) for kernel `kind` (KERNELS)."""
+    def profile_read(self, kind=0, level=None):
+        """(summed kernel ms, launches, cell-timesteps) for kernel `kind`
+        (KERNELS), over all levels or one hierarchy level."""
         ms, n, cells = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
-        _lib.check(self._L.smk_nso_profile_read(self._h, int(kind), ctypes.byref(ms), ctypes.byref(n),
-                                                ctypes.byref(cells)), "profile_read")
+        if level is None:
+            rc = self._L.smk_nso_profile_read(self._h, int(kind), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(cells))
+        else:
+            rc = self._L.smk_nso_profile_read_level(self._h, int(kind), int(level), ctypes.byref(ms), ctypes.byref(n),
+                                                    ctypes.byref(cells))
+        _lib.check(rc, "profile_read")
         return ms.value, n.value, cells.value
 
     def set_guide(self, v0, vstar):

@@ -226,3 +226,16 @@ def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
                     assert rel_err(x, y) < 1e-12
             else:
                 assert rel_err(a, b) < 1e-12
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_kkt_residual_compile_time_extents(nso, n):
+    """The 64^3 / 128^3 Neumann levels run residual kernels with compile-time
+    strides; check them against the oracle at those sizes (fp64, with rhs)."""
+    pb = make_problem(3, n=n, N=2 if n == 64 else 1, seed=61)
+    rng = np.random.default_rng(8)
+    st = random_state(pb, rng)
+    rhs = random_residual(pb, rng)
+    s, cfg = spec_cfg(nso, pb)
+    got = nso.kkt_residual(s, cfg, to_dev(nso, st), pb.v0, pb.vstar, rhs=to_dev_res(nso, rhs))
+    assert res_err(got, stfas.kkt_residual(pb, st).sub(rhs)) < 1e-12
