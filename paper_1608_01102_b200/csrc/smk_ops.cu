@@ -267,36 +267,93 @@ __device__ __forceinline__ void pro_idx(int I, int n, int& i0, int& i1) {
   else i1 = i1 < 0 ? 0 : (i1 > n - 1 ? n - 1 : i1);
 }
 
-// prolong_cell with the reference's axis order (fields.py:256-284)
+// prolong_cell with the reference's axis order (fields.py:256-284).
+// Launch: x over the last (contiguous) axis, y over the rows of the leading
+// axes, z over frames -- the leading-axis coarse rows are block-uniform, so a
+// thread does only its own last-axis weights and 2^d coalesced loads.
+// Prolongation launch shape (cells and faces): one block per kProlongRows fine
+// rows of the leading axes (y) and frame (z); the block stages the 2^(d-1) coarse rows its
+// row interpolates from in shared memory, then every thread builds fine
+// elements along the contiguous axis from them.
+constexpr int kProlongRows = 8;
+
 template <int DIM, bool PER, class R>
 __global__ void k_prolong_cell(Ix<DIM, PER> cx, Ix<DIM, PER> fx, const R* __restrict__ x, R* __restrict__ out,
                                int N, int accumulate) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* crow = reinterpret_cast<R*>(smem_raw);         // [2^(d-1)][cnl]
+  constexpr int NR = DIM == 3 ? 4 : 2;
   const int64_t ncc = cx.cells(), ncf = fx.cells();
   const int fr = blockIdx.z;
-  SMK_FRAME_LOOP(e, ncf) {
-    const int64_t t = (int64_t)fr * ncf + e;
-    int F[3];
-    fx.cell_idx32(e, F);
-    const R* p = x + (int64_t)fr * ncc;
-    int a0, a1, b0, b1, e0 = 0, e1 = 0;
-    pro_idx<PER>(F[0], cx.n0, a0, a1);
-    pro_idx<PER>(F[1], cx.n1, b0, b1);
-    if (DIM == 3) pro_idx<PER>(F[2], cx.n2, e0, e1);
-    R y[2][2];
-    int bj[2] = {b0, b1}, el[2] = {e0, e1};
+  const int nl = DIM == 3 ? fx.n2 : fx.n1, cnl = DIM == 3 ? cx.n2 : cx.n1;
+  const int nrows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
+  const R* p = x + (int64_t)fr * ncc;
+  const int rend = min(nrows, (int)(blockIdx.y + 1) * kProlongRows);
+  for (int row = blockIdx.y * kProlongRows; row < rend; ++row) {
+    const int F0 = DIM == 3 ? row / fx.n1 : row;
+    const int F1 = DIM == 3 ? row - F0 * fx.n1 : 0;
+    int a0, a1, b0 = 0, b1 = 0;
+    pro_idx<PER>(F0, cx.n0, a0, a1);
+    if (DIM == 3) pro_idx<PER>(F1, cx.n1, b0, b1);
+    R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? ((int64_t)F0 * fx.n1 + F1) * fx.n2 : (int64_t)F0 * fx.n1);
+    // the fine row's old values (accumulate) load alongside the coarse rows
+    R old[2] = {R(0), R(0)};
+    if (accumulate) {
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int e = 0; e < (DIM == 3 ? 2 : 1); ++e)
-        y[b][e] = R(0.75) * p[cx.cell_off(a0, bj[b], el[e])] + R(0.25) * p[cx.cell_off(a1, bj[b], el[e])];
-    R z0 = R(0.75) * y[0][0] + R(0.25) * y[1][0];
-    R res = z0;
-    if (DIM == 3) {
-      R z1 = R(0.75) * y[0][1] + R(0.25) * y[1][1];
-      res = R(0.75) * z0 + R(0.25) * z1;
+      for (int u = 0; u < 2; ++u) {
+        const int Fl = threadIdx.x + u * blockDim.x;
+        if (Fl < nl) old[u] = orow[Fl];
+      }
     }
-    out[t] = accumulate ? out[t] + res : res;
+    __syncthreads();   // previous row's readers are done with crow
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? a1 : a0;
+      const int b = DIM == 3 ? ((r & 1) ? b1 : b0) : 0;
+      const R* src = p + (DIM == 3 ? cx.cell_off(a, b, 0) : cx.cell_off(a, 0, 0));
+      for (int l = threadIdx.x; l < cnl; l += blockDim.x) crow[r * cnl + l] = src[l];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int Fl = threadIdx.x + u * blockDim.x;
+      if (Fl >= nl) break;
+      int e0, e1;
+      pro_idx<PER>(Fl, cnl, e0, e1);
+      R res;
+      if (DIM == 3) {
+        // rows: 0 (a0,b0) 1 (a0,b1) 2 (a1,b0) 3 (a1,b1); axis 0, then 1, then 2
+        R y[2][2];
+        const int el[2] = {e0, e1};
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            y[b][e] = R(0.75) * crow[(0 * 2 + b) * cnl + el[e]] + R(0.25) * crow[(1 * 2 + b) * cnl + el[e]];
+        R z0 = R(0.75) * y[0][0] + R(0.25) * y[1][0];
+        R z1 = R(0.75) * y[0][1] + R(0.25) * y[1][1];
+        res = R(0.75) * z0 + R(0.25) * z1;
+      } else {
+        // rows: 0 (a0) 1 (a1); axis 0 then axis 1
+        R y0 = R(0.75) * crow[e0] + R(0.25) * crow[cnl + e0];
+        R y1 = R(0.75) * crow[e1] + R(0.25) * crow[cnl + e1];
+        res = R(0.75) * y0 + R(0.25) * y1;
+      }
+      orow[Fl] = accumulate ? old[u] + res : res;
+    }
   }
+}
+
+template <int DIM, bool PER>
+inline dim3 prolong_cell_grid(const Ix<DIM, PER>& fx, int N, int& tpb) {
+  const int nl = DIM == 3 ? fx.n2 : fx.n1;
+  tpb = nl >= 256 ? 256 : (nl + 31) / 32 * 32;   // <= 2 elements per thread
+  const int rows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
+  return dim3(1, (rows + kProlongRows - 1) / kProlongRows, N);
+}
+template <int DIM, bool PER, class R>
+inline size_t prolong_cell_smem(const Ix<DIM, PER>& cx) {
+  return (size_t)(DIM == 3 ? 4 : 2) * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
 }
 
 // face restriction: along the normal take the coincident (even) face, across
@@ -362,38 +419,81 @@ __device__ __forceinline__ void pro_face_axis(int I, int n_c_axis, bool normal, 
   }
 }
 
+// launch shape as k_prolong_cell, one launch per component k
 template <int DIM, bool PER, class R>
-__global__ void k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, Face3<R> in, FaceW<R> out, int N, int accumulate) {
-  const int k = blockIdx.y;
+__global__ void k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, int k, const R* __restrict__ in, R* __restrict__ out,
+                               int N, int accumulate) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* crow = reinterpret_cast<R*>(smem_raw);         // [2^(d-1)][cnl]
+  constexpr int NR = DIM == 3 ? 4 : 2;
   const int64_t nfc = cx.faces(k), nff = fx.faces(k);
+  const int L = DIM - 1;                             // last (contiguous) axis
+  const int nl = fx.fe(k, L), cnl = cx.fe(k, L);
   const int fr = blockIdx.z;
-  SMK_FRAME_LOOP(e, nff) {
-    const int64_t t = (int64_t)fr * nff + e;
-    int F[3];
-    fx.face_idx32(k, e, F);
-    const R* p = in.c[k] + (int64_t)fr * nfc;
+  const int nrows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
+  const R* p = in + (int64_t)fr * nfc;
+  const int rend = min(nrows, (int)(blockIdx.y + 1) * kProlongRows);
+  for (int row = blockIdx.y * kProlongRows; row < rend; ++row) {
+    int F[3] = {0, 0, 0};
+    if (DIM == 3) {
+      F[0] = row / fx.fe(k, 1);
+      F[1] = row - F[0] * fx.fe(k, 1);
+    } else {
+      F[0] = row;
+    }
     int i0[3], i1[3];
     R w0[3], w1[3];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a >= DIM) { i0[a] = i1[a] = 0; w0[a] = R(1); w1[a] = R(0); continue; }
-      pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
+    for (int a = 0; a < DIM - 1; ++a) pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
+    R* orow = out + (int64_t)fr * nff + fx.face_off(k, F[0], F[1], 0);
+    // the fine row's old values (accumulate) load alongside the coarse rows
+    R old[2] = {R(0), R(0)};
+    if (accumulate) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int Fl = threadIdx.x + u * blockDim.x;
+        if (Fl < nl) old[u] = orow[Fl];
+      }
     }
-    // sequential axis application: y over axis 0, then axis 1, then axis 2.
-    // A weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit.
-    auto ax0 = [&](int j, int l) -> R {
-      R a = p[cx.face_off(k, i0[0], j, l)];
-      if (w1[0] == R(0)) return a;
-      return w0[0] * a + w1[0] * p[cx.face_off(k, i1[0], j, l)];
-    };
-    auto ax1 = [&](int l) -> R {
-      R a = ax0(i0[1], l);
-      if (w1[1] == R(0)) return a;
-      return w0[1] * a + w1[1] * ax0(i1[1], l);
-    };
-    R res = ax1(i0[2]);
-    if (DIM == 3 && w1[2] != R(0)) res = w0[2] * res + w1[2] * ax1(i1[2]);
-    out.c[k][t] = accumulate ? out.c[k][t] + res : res;
+    __syncthreads();   // previous row's readers are done with crow
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? i1[0] : i0[0];
+      const int b = DIM == 3 ? ((r & 1) ? i1[1] : i0[1]) : 0;
+      const R* src = p + cx.face_off(k, a, b, 0);
+      for (int l = threadIdx.x; l < cnl; l += blockDim.x) crow[r * cnl + l] = src[l];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int Fl = threadIdx.x + u * blockDim.x;
+      if (Fl >= nl) break;
+      int il0, il1;
+      R wl0, wl1;
+      pro_face_axis<DIM, PER, R>(Fl, cx.n(L), L == k, il0, il1, wl0, wl1);
+      // sequential axis application: y over axis 0, then axis 1, then axis 2.
+      // A weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit.
+      // Rows: (axis-0 pick, axis-1 pick) -> index a * 2 + b (3D) / a (2D).
+      auto ax0 = [&](int b, int l) -> R {
+        R a = crow[(DIM == 3 ? 0 * 2 + b : 0) * cnl + l];
+        if (w1[0] == R(0)) return a;
+        return w0[0] * a + w1[0] * crow[(DIM == 3 ? 1 * 2 + b : 1) * cnl + l];
+      };
+      R res;
+      if (DIM == 3) {
+        auto ax1 = [&](int l) -> R {
+          R a = ax0(0, l);
+          if (w1[1] == R(0)) return a;
+          return w0[1] * a + w1[1] * ax0(1, l);
+        };
+        res = ax1(il0);
+        if (wl1 != R(0)) res = wl0 * res + wl1 * ax1(il1);
+      } else {
+        res = ax0(0, il0);
+        if (wl1 != R(0)) res = wl0 * res + wl1 * ax0(0, il1);
+      }
+      orow[Fl] = accumulate ? old[u] + res : res;
+    }
   }
 }
 
@@ -736,7 +836,10 @@ template <int DIM, bool PER, class R>
 void launch_prolong_cell(const Geo& gc, int N, const R* x, R* out, int acc, cudaStream_t st) {
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
-  k_prolong_cell<DIM, PER, R><<<frame_grid(fx.cells(), N, 256), 256, 0, st>>>(cx, fx, x, out, N, acc); count_launch();
+  int tpb;
+  const dim3 grid = prolong_cell_grid(fx, N, tpb);
+  k_prolong_cell<DIM, PER, R><<<grid, tpb, prolong_cell_smem<DIM, PER, R>(cx), st>>>(cx, fx, x, out, N, acc);
+  count_launch();
 }
 template <int DIM, bool PER, class R>
 void launch_restrict_face(const Geo& gf, int N, Face3<R> in, FaceW<R> out, cudaStream_t st) {
@@ -749,8 +852,15 @@ template <int DIM, bool PER, class R>
 void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int acc, cudaStream_t st) {
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
-  k_prolong_face<DIM, PER, R><<<frame_grid(fx.faces(0), N, 256, DIM), 256, 0, st>>>(cx, fx, in, out, N, acc);
-  count_launch();
+  for (int k = 0; k < DIM; ++k) {
+    const int nl = fx.fe(k, DIM - 1);
+    const int tpb = nl >= 256 ? 256 : (nl + 31) / 32 * 32;   // <= 2 elements per thread
+    const int rows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
+    const dim3 grid(1, (rows + kProlongRows - 1) / kProlongRows, N);
+    const size_t shm = (size_t)(DIM == 3 ? 4 : 2) * cx.fe(k, DIM - 1) * sizeof(R);
+    k_prolong_face<DIM, PER, R><<<grid, tpb, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
+    count_launch();
+  }
 }
 
 #define SMK_INST(DIM, PER, R)                                                                               \
@@ -952,7 +1062,12 @@ struct PoissonMG {
     Ix<DIM, PER> cx(gc);
     k_resid_restrict<DIM, PER, R><<<grid_for(cx.cells(), 256), 256, 0, st>>>(ix, cx, h, p[li], rhs[li], rhs[li + 1]); count_launch();
     vcycle(li + 1, true, st);
-    k_prolong_cell<DIM, PER, R><<<gb, 256, 0, st>>>(cx, ix, p[li + 1], p[li], 1, 1); count_launch();
+    {
+      int tpb;
+      const dim3 pg = prolong_cell_grid(ix, 1, tpb);
+      k_prolong_cell<DIM, PER, R><<<pg, tpb, prolong_cell_smem<DIM, PER, R>(cx), st>>>(cx, ix, p[li + 1], p[li], 1, 1);
+      count_launch();
+    }
     k_jacobi<DIM, PER, R><<<gb, 256, 0, st>>>(ix, h, om, p[li], rhs[li], tmp[li], 0); count_launch();
     k_jacobi<DIM, PER, R><<<gb, 256, 0, st>>>(ix, h, om, tmp[li], rhs[li], p[li], 0); count_launch();
   }
