@@ -121,6 +121,13 @@ class SpacetimeResidual:
     def zeros(cls, spec, N, dtype=torch.float64):
         return cls(_faces(spec, N, dtype), _cells(spec, N, dtype), _faces(spec, N, dtype), _cells(spec, N, dtype))
 
+    @classmethod
+    def empty(cls, spec, N, dtype=torch.float64):
+        """Uninitialised buffers for a kernel that writes every row."""
+        f = lambda: tuple(torch.empty((N,) + spec.face_shape(k), dtype=dtype, device="cuda") for k in range(spec.dim))
+        c = lambda: torch.empty((N,) + tuple(spec.res), dtype=dtype, device="cuda")
+        return cls(f(), c(), f(), c())
+
     def c_struct(self):
         s = _lib.smk_residual()
         for k, c in enumerate(self.R1):

@@ -58,6 +58,7 @@ class SingleComm:
     """One process holds every slab."""
 
     rank, world = 0, 1
+    host_sync = False
 
     def exchange(self, send_left, send_right, recv_left, recv_right):
         pass
@@ -78,6 +79,11 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # NCCL P2P is ordered on the device (the NCCL stream waits for the
+        # producing kernels, wait() makes the compute stream wait for the
+        # transfer): no host round-trip per exchange.  Host backends (gloo)
+        # read the buffers on the host, so the device work must be finished.
+        self.host_sync = dist.get_backend(group) != "nccl"
 
     @staticmethod
     def _t(x):
@@ -155,7 +161,8 @@ class SlabSolver:
         send_right = E[-1].last_v(states[-1]) if last < self.P - 1 else ()
         recv_left = bufs[0]["vprev"] if first > 0 else ()
         recv_right = bufs[-1]["unext"] if last < self.P - 1 else ()
-        E[0].sync()
+        if getattr(self.comm, "host_sync", True):
+            E[0].sync()
         self.comm.exchange(send_left, send_right, recv_left, recv_right)
         halos = []
         for s in range(S):
@@ -277,7 +284,8 @@ class LibEngine:
 
     # ---- compute ----
     def residual(self, l, st, rhs, halo):
-        out = SpacetimeResidual.zeros(self.specs[l], self.Nl, self.dtype)
+        # k_kkt writes every row (wall rows included), so no zero-fill
+        out = SpacetimeResidual.empty(self.specs[l], self.Nl, self.dtype)
         s, o = st.c_struct(), out.c_struct()
         r = rhs.c_struct() if rhs is not None else None
         rc = self._L.smk_nso_level_residual(self.hier._h, l, ctypes.byref(s), _lib.ptrs(halo.vprev),
