@@ -464,9 +464,13 @@ __device__ __forceinline__ void jac_cached(R c0, R idt, const R (&v)[DIM][NbrSlo
 template <int DIM>
 struct Line {
   static constexpr int NF = 2 * DIM, B = NF + 1;
-  static constexpr int NL = B * (B - 1) / 2;            // strict lower triangle of L
-  static constexpr int L0 = 0, D0 = NL, Z0 = NL + B, Y0 = NL + 2 * B;
-  static constexpr int SE = NL + 3 * B;                  // L, 1/d, z, yu
+  // hand-off of a pair, two formats sharing one scratch stride SE:
+  //   compact (big colours): D~ faces block (lower triangle with diagonal), rhs b, yu
+  //   factored (small, latency-bound colours): L (strict lower), 1/d, z, yu
+  static constexpr int NT = NF * (NF + 1) / 2, NL = B * (B - 1) / 2;
+  static constexpr int T0 = 0, B0 = NT, Y0 = NL + 2 * B;
+  static constexpr int L0 = 0, D0 = NL, Z0 = NL + B;
+  static constexpr int SE = NL + 3 * B;
   static constexpr int NV = DIM * NbrSlots<DIM>::NB;     // V stencil values behind M
   static constexpr int NE = 2 * B + NV;                  // ring entry: yu, yv, V stencil
   static constexpr int E_YU = 0, E_YV = B, E_VS = 2 * B;
@@ -514,7 +518,7 @@ __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
                                                                    : 1;
 }
 
-template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX>
+template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX, bool CMP>
 __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R)))
     k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int o0, int o1, int o2, int mod, int m0, int m1,
                int m2, R* __restrict__ scratch, int* flag) {
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   // solves K' z = [rhs; -ycell].  The coupling to the next pair enters only
   // through Y = L^-1 [P M_{i+1}; 0]:  D~_{i+1} = D_{i+1} - Y^T diag(1/d) Y / dt^2,
   // and the back substitution needs W_i dv = K'^-1 [-P M_{i+1} dv / dt; 0],
-  // so the pair stores (L, 1/d, z) -- no explicit W.
+  // so the pair hands off only D~_i and its rhs -- no explicit W.
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
   // D faces block of pair ip: (PM)^T PM + [ip+1<N] P/dt^2 + alpha / wall identity
   // (lower triangle)
@@ -694,6 +698,30 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     }
     b[NF] = -ycell;
   };
+  // hand-off of pair i to the backward pass: the Schur-updated faces block
+  // (before the saddle is appended and factored) and the pair's rhs; the
+  // backward re-runs the identical factorisation, so this is 35 values per
+  // pair instead of L, 1/d and z (42)
+  auto store_pair = [&](int i, const R (&b)[B]) {
+#pragma unroll
+    for (int r = 0; r < NF; ++r)
+#pragma unroll
+      for (int c = 0; c <= r; ++c) *sc(i, LN::T0 + r * (r + 1) / 2 + c) = T[r][c];
+#pragma unroll
+    for (int r = 0; r < B; ++r) *sc(i, LN::B0 + r) = b[r];
+  };
+  // factored hand-off (small colours): L, 1/d and z of pair i
+  auto store_factors = [&](int i, const R (&dinv)[B], const R (&z)[B]) {
+#pragma unroll
+    for (int r = 1; r < B; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) *sc(i, LN::L0 + r * (r - 1) / 2 + c) = T[r][c];
+#pragma unroll
+    for (int r = 0; r < B; ++r) {
+      *sc(i, LN::D0 + r) = dinv[r];
+      *sc(i, LN::Z0 + r) = z[r];
+    }
+  };
   auto saddle = [&]() {
 #pragma unroll
     for (int a = 0; a < NF; ++a) T[NF][a] = cg.gcol[a];
@@ -705,20 +733,11 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     R b[B], dinv[B], cn[NF];
     c_of(i + 1, cn);
     build_rhs(cn, b);
+    if (CMP && act) store_pair(i, b);
     saddle();
     ok &= ldlt<R, B>(T, dinv, tinyv);
     ldlt_solve<R, B>(T, dinv, b);
-    if (act) {
-#pragma unroll
-      for (int r = 1; r < B; ++r)
-#pragma unroll
-        for (int c = 0; c < r; ++c) *sc(i, LN::L0 + r * (r - 1) / 2 + c) = T[r][c];
-#pragma unroll
-      for (int r = 0; r < B; ++r) {
-        *sc(i, LN::D0 + r) = dinv[r];
-        *sc(i, LN::Z0 + r) = b[r];
-      }
-    }
+    if (!CMP && act) store_factors(i, dinv, b);
     P2 PM[NF][NH];
     mats_of(i + 1, cn, PM, xr, ycell);
 #pragma unroll
@@ -766,6 +785,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 #pragma unroll
     for (int a = 0; a < NF; ++a) cn[a] = R(0);
     build_rhs(cn, b);
+    if (CMP && act) store_pair(i, b);
     saddle();
     if (cx.t0 + i < cx.Ng - 1) {
       R dinv[B];
@@ -775,7 +795,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
       // alpha = 0: D~ is singular along M^-1 g; the saddle is not -> pivot
       ok &= saddle_solve_pivot<R, B>(T, b, tinyv);
     }
-    if (act) {
+    if (!CMP && act) {
 #pragma unroll
       for (int r = 0; r < B; ++r) *sc(i, LN::Z0 + r) = b[r];
     }
@@ -784,26 +804,29 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 }
 
 // Back substitution of one colour, pair i = N-1 .. 0:
-//   dv, dpbar of pair i = z_i - K'_i^-1 [-P M_{i+1} dv_{i+1} / dt; 0]  (stored
-//   L, 1/d of pair i; M_{i+1} recomputed from V), then du, dp of pair i+1
-//   from dv_{i+1}, dv_{i+2}, yu_{i+1} and the same M_{i+1} dv_{i+2}.
+//   refactor pair i's saddle from the handed-off D~ faces block (the same
+//   LDL^T / pivoted solve as the forward pass, so bitwise the same factors),
+//   z_i = K'^-1 b_i, then dv, dpbar of pair i = z_i - K'^-1 [-P M_{i+1} dv_{i+1}/dt; 0]
+//   (M_{i+1} recomputed from V), then du, dp of pair i+1 from dv_{i+1},
+//   dv_{i+2}, yu_{i+1} and the same M_{i+1} dv_{i+2}.
 // Writes omega * deltas to xout [2 * pair + (0: u-block, 1: v-block)][entry][m].
-// PIPE (small colours, latency-bound): the loads of step i-1 (its stored
-// factors, u-rows and V stencil) are issued before step i computes, so one
-// memory latency overlaps one step instead of adding to it.
-template <int DIM, class R>
+// PIPE (small colours, latency-bound): the loads of step i-1 (its hand-off,
+// u-rows and V stencil) are issued before step i computes, so one memory
+// latency overlaps one step instead of adding to it.
+template <int DIM, class R, bool CMP>
 struct BackIn {
-  static constexpr int B = 2 * DIM + 1, NB = NbrSlots<DIM>::NB;
-  R z[B], d[B], l[B * (B - 1) / 2], yu[B];
+  static constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
+  // compact: D~ faces block + rhs; factored: L + 1/d + z
+  R t[CMP ? NF * (NF + 1) / 2 : B * (B - 1) / 2], b[B], d[CMP ? 1 : B], yu[B];
   R VC[DIM][NB];
 };
 
-template <int DIM, bool PER, class R, bool PIPE, int NX>
+template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP>
 __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
                                                    R* __restrict__ xout) {
   using LN = Line<DIM>;
-  constexpr int NF = LN::NF, B = LN::B, NL = LN::NL;
+  constexpr int NF = LN::NF, B = LN::B, NTT = CMP ? LN::NT : LN::NL;
   const auto& ix = cx.ix;
   const int N = cx.N;
   const int64_t M = (int64_t)m0 * m1 * m2;
@@ -813,19 +836,21 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   const auto& cg = lc.cg;
   const Loc<DIM, PER, NX> L(ix, cg.c);
   const R idt = cx.idt;
+  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
-  // inputs of step i: factors and z of pair i; u-rows of pair i+1 and the V
+  // inputs of step i: hand-off of pair i; u-rows of pair i+1 and the V
   // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
-  auto fetch = [&](int i, BackIn<DIM, R>& in) {
+  auto fetch = [&](int i, BackIn<DIM, R, CMP>& in) {
     if (i >= 0) {
+      if (CMP || i + 1 < N) {
 #pragma unroll
-      for (int r = 0; r < B; ++r) {
-        in.z[r] = sc(i, LN::Z0 + r);
-        in.d[r] = sc(i, LN::D0 + r);
+        for (int e = 0; e < NTT; ++e) in.t[e] = sc(i, (CMP ? LN::T0 : LN::L0) + e);
       }
-      if (i + 1 < N) {
 #pragma unroll
-        for (int e = 0; e < NL; ++e) in.l[e] = sc(i, LN::L0 + e);
+      for (int r = 0; r < B; ++r) in.b[r] = sc(i, (CMP ? LN::B0 : LN::Z0) + r);
+      if (!CMP) {
+#pragma unroll
+        for (int r = 0; r < B; ++r) in.d[r] = sc(i, LN::D0 + r);
       }
     }
     if (i + 1 < N) {
@@ -835,7 +860,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
     }
   };
   // t = M dv from a V stencil
-  auto mdot = [&](const BackIn<DIM, R>& in, const R (&dv)[NF], R (&t)[NF]) {
+  auto mdot = [&](const BackIn<DIM, R, CMP>& in, const R (&dv)[NF], R (&t)[NF]) {
     R Mi[NF][NF];
     jac_cached<DIM, R>(cx.c0, idt, in.VC, cg.wall, Mi);
 #pragma unroll
@@ -866,7 +891,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   R t[NF];    // M_{i+1} dv_{i+1}
 #pragma unroll
   for (int q = 0; q < NF; ++q) xn[q] = R(0);
-  BackIn<DIM, R> cur, nxt;
+  BackIn<DIM, R, CMP> cur, nxt;
   if (PIPE) fetch(N - 1, nxt);
   for (int i = N - 1; i >= -1; --i) {
     if (PIPE) {
@@ -875,7 +900,6 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
     } else {
       fetch(i, cur);
     }
-    R xb[B];
     if (i + 1 < N) mdot(cur, xn, t);
     if (i < 0) {
       R zero[NF];
@@ -884,8 +908,33 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       u_delta(0, cur.yu, zero, t);   // dv_0 = 0 (pinned / frozen halo)
       break;
     }
+    R T[B][B], dinv[B], xb[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) xb[r] = cur.z[r];
+    for (int r = 0; r < B; ++r) xb[r] = cur.b[r];
+    if (CMP) {
+      // pair i's saddle, refactored exactly as in the forward pass
+#pragma unroll
+      for (int r = 0; r < NF; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) T[r][c] = cur.t[r * (r + 1) / 2 + c];
+#pragma unroll
+      for (int a = 0; a < NF; ++a) T[NF][a] = cg.gcol[a];
+      T[NF][NF] = R(0);
+      if (i + 1 < N || cx.t0 + i < cx.Ng - 1) {
+        ldlt<R, B>(T, dinv, tinyv);
+        ldlt_solve<R, B>(T, dinv, xb);
+      } else {
+        saddle_solve_pivot<R, B>(T, xb, tinyv);
+      }
+    } else if (i + 1 < N) {
+      // stored factors
+#pragma unroll
+      for (int r = 1; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < r; ++c) T[r][c] = cur.t[r * (r - 1) / 2 + c];
+#pragma unroll
+      for (int r = 0; r < B; ++r) dinv[r] = cur.d[r];
+    }
     if (i + 1 < N) {
       R wf[NF], w[B];
 #pragma unroll
@@ -894,17 +943,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
 #pragma unroll
       for (int q = 0; q < NF; ++q) w[q] = -wf[q] * idt;
       w[NF] = R(0);
-      // K'^-1 w with the stored L, 1/d
-#pragma unroll
-      for (int r = 1; r < B; ++r)
-#pragma unroll
-        for (int c = 0; c < r; ++c) w[r] -= cur.l[r * (r - 1) / 2 + c] * w[c];
-#pragma unroll
-      for (int r = 0; r < B; ++r) w[r] *= cur.d[r];
-#pragma unroll
-      for (int r = B - 2; r >= 0; --r)
-#pragma unroll
-        for (int c = r + 1; c < B; ++c) w[r] -= cur.l[c * (c - 1) / 2 + r] * w[c];
+      ldlt_solve<R, B>(T, dinv, w);   // K'^-1 w
 #pragma unroll
       for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
@@ -1227,11 +1266,11 @@ struct Nso : NsoBase {
     f(std::integral_constant<int, 0>{});
   }
 
-  template <int TM, int P, bool HR, int NX>
+  template <int TM, int P, bool HR, int NX, bool CMP>
   void launch_fwd_t(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, const int o[3], int mod, const int mm[3], int64_t M,
                     cudaStream_t st) {
     const size_t shm = (size_t)ring_stages(P) * Line<DIM>::NE * TM * sizeof(R);
-    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX>;
+    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX, CMP>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -1241,11 +1280,11 @@ struct Nso : NsoBase {
                                                                    scratch, flag);
     count_launch();
   }
-  template <int TM, int P, int NX>
+  template <int TM, int P, int NX, bool CMP>
   void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, bool hr, const int o[3], int mod, const int mm[3],
                   int64_t M, cudaStream_t st) {
-    if (hr) launch_fwd_t<TM, P, true, NX>(c, r, o, mod, mm, M, st);
-    else launch_fwd_t<TM, P, false, NX>(c, r, o, mod, mm, M, st);
+    if (hr) launch_fwd_t<TM, P, true, NX, CMP>(c, r, o, mod, mm, M, st);
+    else launch_fwd_t<TM, P, false, NX, CMP>(c, r, o, mod, mm, M, st);
   }
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
@@ -1270,13 +1309,20 @@ struct Nso : NsoBase {
     // colour cells per SM decide the shape: many -> one producer group
     // (throughput), few -> more producer groups per cell (latency)
     int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
+    // big colours (unpipelined backward) hand off the compact D~ / rhs
+    // format, small latency-bound ones the factored format
+    const bool cmp = M >= back_flat && shape == 0;
     if (shape == 2) {
-      launch_fwd<32, 4, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
+      launch_fwd<32, 4, 0, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
     } else {
       with_nx(l, [&](auto nxc) {
         constexpr int NXv = decltype(nxc)::value;
-        if (shape == 0) launch_fwd<64, 1, NXv>(c, r, rhs != nullptr, o, mod, mm, M, st);
-        else launch_fwd<32, 2, NXv>(c, r, rhs != nullptr, o, mod, mm, M, st);
+        if (shape == 0) {
+          if (cmp) launch_fwd<64, 1, NXv, true>(c, r, rhs != nullptr, o, mod, mm, M, st);
+          else launch_fwd<64, 1, NXv, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
+        } else {
+          launch_fwd<32, 2, NXv, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
+        }
       });
     }
     prof_end(0, st);
@@ -1284,15 +1330,18 @@ struct Nso : NsoBase {
     {
       const int tpb = M >= 148 * 128 ? 128 : 32;
       const unsigned gb = (unsigned)((M + tpb - 1) / tpb);
-      if (M >= back_flat) {
+      if (cmp) {
         with_nx(l, [&](auto nxc) {
           constexpr int NXv = decltype(nxc)::value;
-          k_scgs_back<DIM, PER, R, false, NXv><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                                  (R)prm.omega, scratch, xout);
+          k_scgs_back<DIM, PER, R, false, NXv, true><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
+                                                                        mm[2], (R)prm.omega, scratch, xout);
         });
+      } else if (M >= back_flat) {
+        k_scgs_back<DIM, PER, R, false, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                                     (R)prm.omega, scratch, xout);
       } else {
-        k_scgs_back<DIM, PER, R, true, 0><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                             (R)prm.omega, scratch, xout);
+        k_scgs_back<DIM, PER, R, true, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                                    (R)prm.omega, scratch, xout);
       }
       count_launch();
     }
