@@ -34,6 +34,7 @@ enum { OP_S = 0, OP_J = 1, OP_JT = 2 };
 // launch accounting (gpu_launches in bench.py): every kernel launch site of
 // the library calls count_launch()
 void count_launch(int n = 1);
+long long launch_count();
 
 template <int DIM, bool PER, class R>
 void launch_div(const Geo& g, int N, Face3<R> v, R* out, cudaStream_t st);

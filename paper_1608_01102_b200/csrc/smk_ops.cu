@@ -22,6 +22,7 @@ namespace smk {
 static thread_local char g_err[512] = {0};
 static std::atomic<long long> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;

@@ -1174,6 +1174,8 @@ struct Nso : NsoBase {
     return cuda_check("nso_profile_read");
   }
   ~Nso() override {
+    if (vc_exec) cudaGraphExecDestroy(vc_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     for (int k = 0; k < NKIND; ++k)
       for (auto& e : ev[k]) {
         cudaEventDestroy(e.a);
@@ -1474,10 +1476,52 @@ struct Nso : NsoBase {
     return SMK_OK;
   }
 
+  // One V-cycle is ~1800 launches: it is captured once into a CUDA graph
+  // (on a private stream, so the caller may use the legacy stream) and
+  // replayed; re-captured when the caller's state / guide buffers change.
+  // Profiling runs and SMK_NO_GRAPH=1 launch directly.
+  cudaGraphExec_t vc_exec = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  const void* vc_key[14] = {};
+  long long vc_launches = 0;
+  bool graph_ok = getenv("SMK_NO_GRAPH") == nullptr;
+
   int vcycle(const smk_state* s, cudaStream_t st) override {
     if (!guide_set) { set_error("nso: set_guide not called"); return SMK_ERR_ARG; }
     StP<R> top = from_api(s);
-    vcycle_level(0, top, nullptr, st);
+    if (!graph_ok || prof) {
+      vcycle_level(0, top, nullptr, st);
+      return cuda_check("nso_vcycle");
+    }
+    const void* key[14] = {s->V[0], s->V[1], s->V[2], s->U[0], s->U[1], s->U[2], s->P, s->PB,
+                           top_v0[0], top_v0[1], top_v0[2], top_vs[0], top_vs[1], top_vs[2]};
+    if (!vc_exec || memcmp(key, vc_key, sizeof(key)) != 0) {
+      if (vc_exec) cudaGraphExecDestroy(vc_exec);
+      vc_exec = nullptr;
+      if (!cap_stream && cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        graph_ok = false;
+        return vcycle(s, st);
+      }
+      const long long n0 = launch_count();
+      cudaGraph_t g = nullptr;
+      bool ok_cap = cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (ok_cap) vcycle_level(0, top, nullptr, cap_stream);
+      ok_cap = ok_cap && cudaStreamEndCapture(cap_stream, &g) == cudaSuccess && g;
+      ok_cap = ok_cap && cudaGraphInstantiate(&vc_exec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      if (!ok_cap) {
+        cudaGetLastError();
+        vc_exec = nullptr;
+        graph_ok = false;
+        return vcycle(s, st);
+      }
+      vc_launches = launch_count() - n0;   // counted once while capturing
+      memcpy(vc_key, key, sizeof(key));
+    } else {
+      count_launch((int)vc_launches);
+    }
+    cudaGraphLaunch(vc_exec, st);
     return cuda_check("nso_vcycle");
   }
 
