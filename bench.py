@@ -132,7 +132,7 @@ def cpu_sample_shape(w):
 
 
 def cpu_vcycle_rate(w, steps=1):
-    """Time the oracle (numpy fp64 port) V-cycle on the host; cell-updates/s."""
+    """Time the oracle (numpy fp64 port) V-cycle on one host core; cell-updates/s."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     from oracle import stfas
     from problems import make_problem
@@ -148,28 +148,55 @@ def cpu_vcycle_rate(w, steps=1):
     return cts / dt, dt, sh
 
 
+def _cpu_worker(args):
+    """One host core: `steps` oracle V-cycles of the bounded sample (BLAS
+    pinned to one thread so the cores are not oversubscribed)."""
+    w, steps = args
+    try:
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(1):
+            return cpu_vcycle_rate(w, steps)
+    except ImportError:
+        return cpu_vcycle_rate(w, steps)
+
+
+def cpu_parallel_rate(w, steps=1, workers=None):
+    """Throughput of the oracle V-cycle on all host cores: one independent
+    sample problem per core (the metric is a throughput), aggregate
+    cell-timesteps / wall time.  Returns (rate, wall_s_per_step, shape, cores)."""
+    import multiprocessing as mp
+    n = workers or max(1, min(os.cpu_count() or 1, 64))
+    if n == 1:
+        r, dt, sh = cpu_vcycle_rate(w, steps)
+        return r, dt, sh, 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(n) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_worker, [(w, steps)] * n)
+        wall = (time.perf_counter() - t0) / steps
+    sh = res[0][2]
+    cts = sh["n"] ** sh["dim"] * sh["N"]
+    return n * cts / wall, wall, sh, n
+
+
 def run_reference(args, w, rank, world):
     if rank != 0:
         return 0
     steps, warm = args.steps, args.warmup
-    rate_s = []
-    sh = None
-    for i in range(warm + steps):
-        r, dt, sh = cpu_vcycle_rate(w, 1)
-        if i >= warm:
-            rate_s.append((r, dt))
-    val = sum(r for r, _ in rate_s) / len(rate_s)
-    ms = 1000.0 * sum(d for _, d in rate_s) / len(rate_s)
-    sample = (f"oracle fp64 numpy FAS V-cycle on a same-family {sh['n']}^{sh['dim']} x {sh['N']} "
-              f"({sh['levels']} levels) problem; rate per cell-timestep")
+    # warm-up: imports, problem construction and the first V-cycle per core
+    cpu_parallel_rate(w, 1) if warm else None
+    rate, wall, sh, cores = cpu_parallel_rate(w, steps)
+    sample = (f"oracle fp64 numpy FAS V-cycle (CPU port of the path; the reference ships no STFAS) on a "
+              f"same-family {sh['n']}^{sh['dim']} x {sh['N']} ({sh['levels']} levels) problem, one independent "
+              f"problem per core on {cores} cores, aggregate rate per cell-timestep")
     line = {
-        "impl": "reference", "metric": "STFAS spacetime cell-updates/s (per V-cycle)", "value": val,
-        "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": ms,
+        "impl": "reference", "metric": "STFAS spacetime cell-updates/s (per V-cycle)", "value": rate,
+        "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * wall,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "config_index": w.index, "cell_timesteps": w.cell_timesteps,
-                   "parallelism": "cpu"},
-        "cpu_baseline": {"value": val, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": sample},
-        "e2e": {"value": val, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "parallelism": f"cpu x{cores}"},
+        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -347,10 +374,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, dt, sh = cpu_vcycle_rate(w, 1)
-            cpu = {"value": rate, "unit": "cell-updates/s", "cores": 1, "kind": "port",
+            rate, dt, sh, cores = cpu_parallel_rate(w, 1)
+            cpu = {"value": rate, "unit": "cell-updates/s", "cores": cores, "kind": "port",
                    "sample": f"oracle fp64 numpy V-cycle, same-family {sh['n']}^{sh['dim']} x {sh['N']} "
-                             f"({sh['levels']} levels), {dt:.1f} s; numpy stencils single-threaded"}
+                             f"({sh['levels']} levels), one problem per core on {cores} cores, {dt:.1f} s wall"}
         except Exception as ex:  # never fail the GPU line on the CPU leg
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
 
