@@ -962,13 +962,18 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
 }
 
 // x += omega * dx on the colour's unknowns (disjoint across cells)
-template <int DIM, bool PER, class R>
-__global__ void k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, int N, int o0, int o1, int o2, int mod, int m0, int m1, int m2,
-                             const R* __restrict__ xout) {
+// x += omega * dx on the colour's unknowns (disjoint across cells); the
+// cell's face / cell offsets are computed once, FPT frames (blockIdx.z +
+// u * gridDim.z) per thread (FPT = 1 measured fastest: more frames per
+// thread strides the same offsets 8 MB apart and lost bandwidth).
+template <int DIM, bool PER, class R, int FPT>
+__global__ void __launch_bounds__(256) k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, int N, int o0, int o1, int o2, int mod,
+                                                    int m0, int m1, int m2, const R* __restrict__ xout) {
   constexpr int NF = 2 * DIM, B = NF + 1;
   const int64_t M = (int64_t)m0 * m1 * m2;
-  int64_t nf[3] = {ix.faces(0), ix.faces(1), DIM == 3 ? ix.faces(2) : 0};
-  const int i = blockIdx.z;
+  const int64_t nf[3] = {ix.faces(0), ix.faces(1), DIM == 3 ? ix.faces(2) : 0};
+  const int64_t ncl = ix.cells();
+  const int fstride = gridDim.z;
   SMK_FRAME_LOOP(m, M) {
     int c[3];
     int q = m;
@@ -977,25 +982,40 @@ __global__ void k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, int N, int o0, int o1, i
     c[0] = o0 + mod * q;
     c[1] = o1 + mod * q1;
     c[2] = DIM == 3 ? o2 + mod * q2 : 0;
-    const R* xu = xout + (int64_t)(2 * i) * B * M + m;
-    const R* xv = xout + (int64_t)(2 * i + 1) * B * M + m;
+    int64_t fo[NF];
+    bool w[NF];
 #pragma unroll
     for (int k = 0; k < DIM; ++k)
 #pragma unroll
       for (int sd = 0; sd < 2; ++sd) {
-        int qq = 2 * k + sd;
-        bool w = !PER && (sd == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
-        if (w) continue;
+        const int qq = 2 * k + sd;
+        w[qq] = !PER && (sd == 0 ? c[k] == 0 : c[k] == ix.n(k) - 1);
         int f[3] = {c[0], c[1], c[2]};
         f[k] += sd;
         if (PER && f[k] >= ix.n(k)) f[k] -= ix.n(k);
-        int64_t o = (int64_t)i * nf[k] + ix.face_off(k, f[0], f[1], f[2]);
-        s.U[k][o] += xu[(int64_t)qq * M];
-        s.V[k][o] += xv[(int64_t)qq * M];
+        fo[qq] = ix.face_off(k, f[0], f[1], f[2]);
       }
-    int64_t oc = (int64_t)i * ix.cells() + ix.cell_off(c[0], c[1], c[2]);
-    s.P[oc] += xu[(int64_t)NF * M];
-    s.PB[oc] += xv[(int64_t)NF * M];
+    const int64_t co = ix.cell_off(c[0], c[1], c[2]);
+#pragma unroll
+    for (int u = 0; u < FPT; ++u) {
+      const int i = blockIdx.z + u * fstride;
+      if (i >= N) break;
+      const R* xu = xout + (int64_t)(2 * i) * B * M + m;
+      const R* xv = xout + (int64_t)(2 * i + 1) * B * M + m;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k)
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+          const int qq = 2 * k + sd;
+          if (w[qq]) continue;
+          const int64_t o = (int64_t)i * nf[k] + fo[qq];
+          s.U[k][o] += xu[(int64_t)qq * M];
+          s.V[k][o] += xv[(int64_t)qq * M];
+        }
+      const int64_t oc = (int64_t)i * ncl + co;
+      s.P[oc] += xu[(int64_t)NF * M];
+      s.PB[oc] += xv[(int64_t)NF * M];
+    }
   }
 }
 
@@ -1097,6 +1117,7 @@ struct Nso : NsoBase {
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
     if (const char* e = getenv("SMK_BACK_FLAT")) back_flat = atoll(e);
+
     if (const char* e = getenv("SMK_FWD_THRESH")) {
       long long a = 0, b = 0;
       if (sscanf(e, "%lld,%lld", &a, &b) == 2) {
@@ -1349,8 +1370,8 @@ struct Nso : NsoBase {
     }
     prof_end(3, st);
     prof_begin(1, l, M, st);
-    k_scgs_apply<DIM, PER, R><<<frame_grid(M, prm.n_frames, 256), 256, 0, st>>>(ix, s, prm.n_frames, o[0], o[1], o[2],
-                                                                                 mod, mm[0], mm[1], mm[2], xout);
+    k_scgs_apply<DIM, PER, R, 1><<<frame_grid(M, prm.n_frames, 256), 256, 0, st>>>(
+        ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], xout);
     count_launch();
     prof_end(1, st);
 
