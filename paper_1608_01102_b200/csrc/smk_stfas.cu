@@ -474,7 +474,16 @@ struct Line {
   static constexpr int NV = DIM * NbrSlots<DIM>::NB;     // V stencil values behind M
   static constexpr int NE = 2 * B + NV;                  // ring entry: yu, yv, V stencil
   static constexpr int E_YU = 0, E_YV = B, E_VS = 2 * B;
+  // prep ring entry (latency-bound shapes: the producers also build the
+  // pair's dense inputs): c, yv + M^T c, dpbar-row rhs, P M, D faces block
+  static constexpr int NEP = 2 * NF + 1 + NF * NF + NT;
+  static constexpr int P_C = 0, P_XR = NF, P_YC = 2 * NF, P_PM = 2 * NF + 1, P_D = 2 * NF + 1 + NF * NF;
 };
+
+// the consumer's dense inputs are built by the producers on the P = 4 shape
+__host__ __device__ constexpr bool fwd_prep(int P) { return P == 4; }
+template <int DIM>
+__host__ __device__ constexpr int fwd_ring_entry(int P) { return fwd_prep(P) ? Line<DIM>::NEP : Line<DIM>::NE; }
 
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) {
@@ -506,6 +515,76 @@ struct LineCell {
   }
 };
 
+// dense per-pair inputs of the time-line elimination (used by the consumer,
+// or by the producers in prep mode); FFMA2 lane pairs over columns 2h, 2h+1
+template <int DIM, bool PER, class R>
+struct PairAlg {
+  static constexpr int NF = 2 * DIM, B = NF + 1, NH = NF / 2, NB = NbrSlots<DIM>::NB;
+  using P2 = R2<R>;
+  __device__ __forceinline__ static R lo_hi(const P2& v, int e) { return e ? v.y : v.x; }
+  // c = P yu + g yu_p / sigma
+  __device__ __forceinline__ static void cvec(const LineCell<DIM, PER, R>& lc, const R (&yu)[B], R (&cv)[NF]) {
+#pragma unroll
+    for (int q = 0; q < NF; ++q) cv[q] = yu[q];
+    lc.projP(cv);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) cv[q] += lc.cg.gcol[q] * yu[NF] * lc.isig;
+  }
+  // M from the V stencil, then P M (column pairs) and xr = yv + M^T c
+  __device__ __forceinline__ static void mats(const LineCell<DIM, PER, R>& lc, R c0, R idt, const R (&VC)[DIM][NB],
+                                              const R (&yv)[B], const R (&cv)[NF], P2 (&PM)[NF][NH],
+                                              R (&xr)[NF]) {
+    const auto& cg = lc.cg;
+    R Mx[NF][NF];
+    jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
+    P2 Mp[NF][NH];
+#pragma unroll
+    for (int t = 0; t < NF; ++t)
+#pragma unroll
+      for (int h = 0; h < NH; ++h) Mp[t][h] = p2(Mx[t][2 * h], Mx[t][2 * h + 1]);
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      P2 s2 = p2(yv[2 * h], yv[2 * h + 1]);
+#pragma unroll
+      for (int t = 0; t < NF; ++t) s2 = fma2s(cv[t], Mp[t][h], s2);
+      xr[2 * h] = s2.x;
+      xr[2 * h + 1] = s2.y;
+    }
+    // P M column pairs: d = isig g^T M, PM = M - g d on the unknown rows
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+      P2 d = p2(R(0), R(0));
+#pragma unroll
+      for (int q = 0; q < NF; ++q) d = fma2s(cg.gcol[q], Mp[q][h], d);
+      d = mul2s(lc.isig, d);
+#pragma unroll
+      for (int a = 0; a < NF; ++a) PM[a][h] = cg.wall[a] ? p2(R(0), R(0)) : fma2s(-cg.gcol[a], d, Mp[a][h]);
+    }
+  }
+  // D faces block (lower triangle): (PM)^T PM + [nx] P/dt^2 + alpha / wall identity
+  __device__ __forceinline__ static void diag(const LineCell<DIM, PER, R>& lc, const R (&gs)[NF], R idt2, R alpha,
+                                              bool nx, const P2 (&PM)[NF][NH], R (&T)[B][B]) {
+    const auto& cg = lc.cg;
+#pragma unroll
+    for (int a = 0; a < NF; ++a)
+#pragma unroll
+      for (int h = 0; h <= (a >> 1); ++h) {
+        P2 acc = p2(R(0), R(0));
+#pragma unroll
+        for (int t = 0; t < NF; ++t) acc = fma2s(lo_hi(PM[t][a >> 1], a & 1), PM[t][h], acc);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int b = 2 * h + e;
+          if (b > a) continue;
+          R s = lo_hi(acc, e);
+          if (nx) s -= cg.gcol[a] * gs[b];
+          if (a == b) s += cg.wall[a] ? R(1) : alpha + (nx ? idt2 : R(0));
+          T[a][b] = s;
+        }
+      }
+  }
+};
+
 // ring stages for P producer groups: a multiple of P, at least 3
 __host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P == 2 ? 4 : P); }
 
@@ -523,7 +602,10 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int o0, int o1, int o2, int mod, int m0, int m1,
                int m2, R* __restrict__ scratch, int* flag) {
   using LN = Line<DIM>;
-  constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB, NE = LN::NE;
+  using PA = PairAlg<DIM, PER, R>;
+  constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB;
+  constexpr bool PREP = fwd_prep(P);
+  constexpr int NE = fwd_ring_entry<DIM>(P);
   constexpr int S = ring_stages(P);
   constexpr int NT = 2 * TM;   // threads per named barrier: one producer group + the consumers
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -542,6 +624,11 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   const R idt = cx.idt;
   auto sc = [&](int i, int e) -> R* { return scratch + ((int64_t)i * LN::SE + e) * M + m; };
   auto slot = [&](int i, int e) -> R* { return ring + ((i % S) * NE + e) * TM + lane; };
+  const R idt2 = idt * idt;
+  R gs[NF];   // g * idt^2 / sigma: P idt^2 = idt^2 I - g gs^T on the unknown faces
+#pragma unroll
+  for (int q = 0; q < NF; ++q) gs[q] = cg.gcol[q] * lc.isig * idt2;
+  auto alpha_of = [&](int ip) -> R { return (cx.t0 + ip < cx.Ng - 1) ? cx.kr : R(0); };
 
   if (producer) {
     const Loc<DIM, PER, NX> L(ix, cg.c);
@@ -573,15 +660,40 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 #pragma unroll
           for (int q = 0; q < NF; ++q) vp[q] = VC[q >> 1][(q & 1) + 1];
         }
+        if constexpr (PREP) {
+          R cv[NF], xrv[NF], Dl[B][B];
+          typename PA::P2 PM[NF][NF / 2];
+          PA::cvec(lc, yu, cv);
+          PA::mats(lc, c0, idt, VC, yv, cv, PM, xrv);
+          PA::diag(lc, gs, idt2, alpha_of(i), i + 1 < N, PM, Dl);
 #pragma unroll
-        for (int q = 0; q < B; ++q) {
-          *slot(i, LN::E_YU + q) = yu[q];
-          *slot(i, LN::E_YV + q) = yv[q];
+          for (int q = 0; q < NF; ++q) {
+            *slot(i, LN::P_C + q) = cv[q];
+            *slot(i, LN::P_XR + q) = xrv[q];
+          }
+          *slot(i, LN::P_YC) = yv[NF];
+#pragma unroll
+          for (int a = 0; a < NF; ++a)
+#pragma unroll
+            for (int h = 0; h < NF / 2; ++h) {
+              *slot(i, LN::P_PM + a * NF + 2 * h) = PM[a][h].x;
+              *slot(i, LN::P_PM + a * NF + 2 * h + 1) = PM[a][h].y;
+            }
+#pragma unroll
+          for (int a = 0; a < NF; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) *slot(i, LN::P_D + a * (a + 1) / 2 + b) = Dl[a][b];
+        } else {
+#pragma unroll
+          for (int q = 0; q < B; ++q) {
+            *slot(i, LN::E_YU + q) = yu[q];
+            *slot(i, LN::E_YV + q) = yv[q];
+          }
+#pragma unroll
+          for (int a = 0; a < DIM; ++a)
+#pragma unroll
+            for (int sl = 0; sl < NB; ++sl) *slot(i, LN::E_VS + a * NB + sl) = VC[a][sl];
         }
-#pragma unroll
-        for (int a = 0; a < DIM; ++a)
-#pragma unroll
-          for (int sl = 0; sl < NB; ++sl) *slot(i, LN::E_VS + a * NB + sl) = VC[a][sl];
       }
       nb_arrive(1 + i % S, NT);   // FULL
     }
@@ -596,12 +708,6 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   // and the back substitution needs W_i dv = K'^-1 [-P M_{i+1} dv / dt; 0],
   // so the pair hands off only D~_i and its rhs -- no explicit W.
   const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
-  // D faces block of pair ip: (PM)^T PM + [ip+1<N] P/dt^2 + alpha / wall identity
-  // (lower triangle)
-  const R idt2 = idt * idt;
-  R gs[NF];   // g * idt^2 / sigma: P idt^2 = idt^2 I - g gs^T on the unknown faces
-#pragma unroll
-  for (int q = 0; q < NF; ++q) gs[q] = cg.gcol[q] * lc.isig * idt2;
   // The dense block algebra below runs on lane pairs (columns 2h, 2h+1):
   // FFMA2 with a broadcast scalar in fp32, each lane rounded exactly like the
   // scalar FFMA of the same expression (same operand order, same summation
@@ -609,69 +715,50 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   constexpr int NH = NF / 2;
   using P2 = R2<R>;
   auto lo_hi = [](const P2& v, int e) -> R { return e ? v.y : v.x; };
+  // D faces block of pair ip (lower triangle)
   auto diag_block = [&](int ip, const P2 (&PM)[NF][NH], R (&T)[B][B]) {
-    const bool nx = ip + 1 < N;
-    const R alpha = (cx.t0 + ip < cx.Ng - 1) ? cx.kr : R(0);
+    if constexpr (PREP) {
 #pragma unroll
-    for (int a = 0; a < NF; ++a)
+      for (int a = 0; a < NF; ++a)
 #pragma unroll
-      for (int h = 0; h <= (a >> 1); ++h) {
-        P2 acc = p2(R(0), R(0));
-#pragma unroll
-        for (int t = 0; t < NF; ++t) acc = fma2s(lo_hi(PM[t][a >> 1], a & 1), PM[t][h], acc);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int b = 2 * h + e;
-          if (b > a) continue;
-          R s = lo_hi(acc, e);
-          if (nx) s -= cg.gcol[a] * gs[b];
-          if (a == b) s += cg.wall[a] ? R(1) : alpha + (nx ? idt2 : R(0));
-          T[a][b] = s;
-        }
-      }
-  };
-  // c = P yu + g yu_p / sigma of pair i (from the ring)
-  auto c_of = [&](int i, R (&cv)[NF]) {
-#pragma unroll
-    for (int q = 0; q < NF; ++q) cv[q] = *slot(i, LN::E_YU + q);
-    lc.projP(cv);
-    const R yp = *slot(i, LN::E_YU + NF);
-#pragma unroll
-    for (int q = 0; q < NF; ++q) cv[q] += cg.gcol[q] * yp * lc.isig;
-  };
-  // M_i from the V stencil, then P M_i, the partial rhs yv + M^T c and the
-  // dpbar-row rhs of pair i
-  auto mats_of = [&](int i, const R (&cv)[NF], P2 (&PM)[NF][NH], R (&xrr)[NF], R& yc) {
-    R VC[DIM][NB];
-#pragma unroll
-    for (int a = 0; a < DIM; ++a)
-#pragma unroll
-      for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(i, LN::E_VS + a * NB + sl);
-    R Mx[NF][NF];
-    jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
-    P2 Mp[NF][NH];
-#pragma unroll
-    for (int t = 0; t < NF; ++t)
-#pragma unroll
-      for (int h = 0; h < NH; ++h) Mp[t][h] = p2(Mx[t][2 * h], Mx[t][2 * h + 1]);
-#pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      P2 s2 = p2(*slot(i, LN::E_YV + 2 * h), *slot(i, LN::E_YV + 2 * h + 1));
-#pragma unroll
-      for (int t = 0; t < NF; ++t) s2 = fma2s(cv[t], Mp[t][h], s2);
-      xrr[2 * h] = s2.x;
-      xrr[2 * h + 1] = s2.y;
+        for (int b = 0; b <= a; ++b) T[a][b] = *slot(ip, LN::P_D + a * (a + 1) / 2 + b);
+    } else {
+      PA::diag(lc, gs, idt2, alpha_of(ip), ip + 1 < N, PM, T);
     }
-    yc = *slot(i, LN::E_YV + NF);
-    // P M column pairs: d = isig g^T M, PM = M - g d on the unknown rows
+  };
+  // c = P yu + g yu_p / sigma of pair i
+  auto c_of = [&](int i, R (&cv)[NF]) {
+    if constexpr (PREP) {
 #pragma unroll
-    for (int h = 0; h < NH; ++h) {
-      P2 d = p2(R(0), R(0));
+      for (int q = 0; q < NF; ++q) cv[q] = *slot(i, LN::P_C + q);
+    } else {
+      R yu[B];
 #pragma unroll
-      for (int q = 0; q < NF; ++q) d = fma2s(cg.gcol[q], Mp[q][h], d);
-      d = mul2s(lc.isig, d);
+      for (int q = 0; q < B; ++q) yu[q] = *slot(i, LN::E_YU + q);
+      PA::cvec(lc, yu, cv);
+    }
+  };
+  // P M_i, the partial rhs yv + M^T c and the dpbar-row rhs of pair i
+  auto mats_of = [&](int i, const R (&cv)[NF], P2 (&PM)[NF][NH], R (&xrr)[NF], R& yc) {
+    if constexpr (PREP) {
 #pragma unroll
-      for (int a = 0; a < NF; ++a) PM[a][h] = cg.wall[a] ? p2(R(0), R(0)) : fma2s(-cg.gcol[a], d, Mp[a][h]);
+      for (int q = 0; q < NF; ++q) xrr[q] = *slot(i, LN::P_XR + q);
+      yc = *slot(i, LN::P_YC);
+#pragma unroll
+      for (int a = 0; a < NF; ++a)
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+          PM[a][h] = p2(*slot(i, LN::P_PM + a * NF + 2 * h), *slot(i, LN::P_PM + a * NF + 2 * h + 1));
+    } else {
+      R VC[DIM][NB], yv[B];
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(i, LN::E_VS + a * NB + sl);
+#pragma unroll
+      for (int q = 0; q < B; ++q) yv[q] = *slot(i, LN::E_YV + q);
+      PA::mats(lc, c0, idt, VC, yv, cv, PM, xrr);
+      yc = yv[NF];
     }
   };
   R T[B][B];      // lower triangle: D~ of the current pair, then its L
@@ -1292,7 +1379,7 @@ struct Nso : NsoBase {
   template <int TM, int P, bool HR, int NX, bool CMP>
   void launch_fwd_t(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, const int o[3], int mod, const int mm[3], int64_t M,
                     cudaStream_t st) {
-    const size_t shm = (size_t)ring_stages(P) * Line<DIM>::NE * TM * sizeof(R);
+    const size_t shm = (size_t)ring_stages(P) * fwd_ring_entry<DIM>(P) * TM * sizeof(R);
     auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX, CMP>;
     static bool attr = false;
     if (!attr) {
