@@ -592,9 +592,11 @@ __host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P ==
 // (group p builds pairs i = p mod P, so the coarse levels -- few cells, long
 // time lines -- get P-fold producer parallelism), one consumer group.
 // resident CTAs per SM the register budget is sized for
+__host__ __device__ constexpr int fwd_min_blocks_f32(int TM, int P) {
+  return P == 1 ? 512 / (2 * TM) : (P == 2 ? 5 : 2);   // 128 registers on P <= 2 (more CTAs spill: measured slower)
+}
 __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
-  return (P == 1 ? 4 : (P == 2 ? 5 : 2)) / (esz == 8 ? 2 : 1) > 0 ? (P == 1 ? 4 : (P == 2 ? 5 : 2)) / (esz == 8 ? 2 : 1)
-                                                                   : 1;
+  return esz == 8 ? (fwd_min_blocks_f32(TM, P) / 2 > 0 ? fwd_min_blocks_f32(TM, P) / 2 : 1) : fwd_min_blocks_f32(TM, P);
 }
 
 template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX, bool CMP>
