@@ -262,6 +262,20 @@ struct Loc {
     int o = of[2 * k] + d0 * fstride(ix, k, 0) + d1 * fstride(ix, k, 1) + (DIM == 3 ? d2 : 0);
     return v ? __ldg(p + o) : R(0);
   }
+  // address and in-range flag of the face read at offset d (for async copies)
+  template <class R>
+  __device__ __forceinline__ const R* face_ptr(const Ix<DIM, PER>& ix, const R* p, int k, int d0, int d1, int d2,
+                                               bool& v) const {
+    if (PER) {
+      v = true;
+      int i = Ix<DIM, PER>::wrap(c[0] + d0, ix.n0), j = Ix<DIM, PER>::wrap(c[1] + d1, ix.n1);
+      int l = DIM == 3 ? Ix<DIM, PER>::wrap(c[2] + d2, ix.n2) : 0;
+      return p + ix.face_off(k, i, j, l);
+    }
+    v = ok(0, d0, k == 0 ? 2 : 1) && ok(1, d1, k == 1 ? 2 : 1) && (DIM == 2 || ok(2, d2, k == 2 ? 2 : 1));
+    int o = of[2 * k] + d0 * fstride(ix, k, 0) + d1 * fstride(ix, k, 1) + (DIM == 3 ? d2 : 0);
+    return v ? p + o : p;
+  }
   template <class R>
   __device__ __forceinline__ R cell(const Ix<DIM, PER>& ix, const R* __restrict__ p, int d0, int d1, int d2) const {
     if (PER) return ix.cell(p, c[0] + d0, c[1] + d1, c[2] + d2);
@@ -447,6 +461,20 @@ __device__ __forceinline__ double2 fma2s(double a, double2 b, double2 c) {
 }
 __device__ __forceinline__ float2 mul2s(float a, float2 b) { return __fmul2_rn(make_float2(a, a), b); }
 __device__ __forceinline__ double2 mul2s(double a, double2 b) { return make_double2(a * b.x, a * b.y); }
+
+// one element global -> shared, asynchronous (cp.async, L1-allocating);
+// valid == false zero-fills (src-size 0) without reading the source
+template <class R>
+__device__ __forceinline__ void cp_async_elem(R* smem, const R* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  if constexpr (sizeof(R) == 4)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 4 : 0) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
 
 // explicit-width |x| (an unqualified abs() on a float can bind to int abs)
 __device__ __forceinline__ float rabs(float x) { return fabsf(x); }

@@ -1050,6 +1050,167 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   }
 }
 
+// Back substitution for small, latency-bound colours (factored hand-off):
+// one warp per 32 cells, and every thread streams its steps' inputs -- the
+// stored factors, u-rows and V stencil, 78 values in 3D -- through a DEPTH-
+// stage shared-memory ring filled by cp.async, DEPTH-1 steps ahead of the
+// serial recursion (zero-filled out-of-domain stencil reads, like Loc::face).
+// Same arithmetic as k_scgs_back<..., PIPE, ..., factored>.
+template <int DIM>
+struct BackDeep {
+  static constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
+  static constexpr int NL = B * (B - 1) / 2;
+  static constexpr int V_T = 0, V_B = NL, V_D = NL + B, V_Y = NL + 2 * B, V_VC = NL + 3 * B;
+  static constexpr int NV = NL + 3 * B + DIM * NB;    // values per step
+};
+template <class R>
+__host__ __device__ constexpr int back_depth() { return sizeof(R) == 4 ? 4 : 2; }
+
+template <int DIM, bool PER, class R>
+__global__ void __launch_bounds__(32) k_scgs_back_deep(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod,
+                                                       int m0, int m1, int m2, R omega,
+                                                       const R* __restrict__ scratch, R* __restrict__ xout) {
+  using LN = Line<DIM>;
+  using BD = BackDeep<DIM>;
+  constexpr int NF = LN::NF, B = LN::B, NB = BD::NB, NV = BD::NV;
+  constexpr int DEPTH = back_depth<R>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* ring = reinterpret_cast<R*>(smem_raw);   // [DEPTH][NV][32]
+  const auto& ix = cx.ix;
+  const int N = cx.N;
+  const int64_t M = (int64_t)m0 * m1 * m2;
+  const int lane = threadIdx.x;
+  const int64_t m = (int64_t)blockIdx.x * 32 + lane;
+  if (m >= M) return;   // no block-wide synchronisation below
+  const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
+  const auto& cg = lc.cg;
+  const Loc<DIM, PER> L(ix, cg.c);
+  const R idt = cx.idt;
+  auto gsc = [&](int i, int e) -> const R* { return scratch + ((int64_t)i * LN::SE + e) * M + m; };
+  auto slot = [&](int stage, int v) -> R* { return ring + (stage * NV + v) * 32 + lane; };
+  // step s handles pair i = N - 1 - s (s = N: only pair 0's u-block)
+  auto issue = [&](int st) {
+    const int i = N - 1 - st;
+    if (i >= -1) {
+      const int stage = st % DEPTH;
+      if (i >= 0) {
+        if (i + 1 < N) {
+#pragma unroll
+          for (int e = 0; e < BD::NL; ++e) cp_async_elem(slot(stage, BD::V_T + e), gsc(i, LN::L0 + e), true);
+#pragma unroll
+          for (int r = 0; r < B; ++r) cp_async_elem(slot(stage, BD::V_D + r), gsc(i, LN::D0 + r), true);
+        }
+#pragma unroll
+        for (int r = 0; r < B; ++r) cp_async_elem(slot(stage, BD::V_B + r), gsc(i, LN::Z0 + r), true);
+      }
+      if (i + 1 < N) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) cp_async_elem(slot(stage, BD::V_Y + q), gsc(i + 1, LN::Y0 + q), true);
+        const Face3<R> Vf = frame_of(cx.V, i + 1, cx.nf);
+#pragma unroll
+        for (int a = 0; a < DIM; ++a)
+#pragma unroll
+          for (int sl = 0; sl < NB; ++sl) {
+            int d[3];
+            NbrSlots<DIM>::offset(a, sl, d);
+            bool v;
+            const R* src = L.face_ptr(ix, Vf.c[a], a, d[0], d[1], d[2], v);
+            cp_async_elem(slot(stage, BD::V_VC + a * NB + sl), src, v);
+          }
+      }
+    }
+    cp_async_commit();   // one group per step (empty past the end)
+  };
+  auto mdot = [&](const R (&VC)[DIM][NB], const R (&dv)[NF], R (&t)[NF]) {
+    R Mi[NF][NF];
+    jac_cached<DIM, R>(cx.c0, idt, VC, cg.wall, Mi);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      R s = R(0);
+#pragma unroll
+      for (int k = 0; k < NF; ++k) s += Mi[q][k] * dv[k];
+      t[q] = s;
+    }
+  };
+  auto u_delta = [&](int ip, const R (&yu)[B], const R (&dvi)[NF], const R (&t)[NF]) {
+    R a[NF];
+    R ga = R(0);
+#pragma unroll
+    for (int q = 0; q < NF; ++q) {
+      R s = yu[q] + dvi[q] * idt - t[q];
+      a[q] = cg.wall[q] ? R(0) : s;
+      ga += cg.gcol[q] * a[q];
+    }
+    const R dp = (ga - yu[NF]) * lc.isig;
+    R* xo = xout + (int64_t)(2 * ip) * B * M + m;
+#pragma unroll
+    for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
+    xo[(int64_t)NF * M] = omega * dp;
+  };
+#pragma unroll
+  for (int st = 0; st < DEPTH - 1; ++st) issue(st);
+  R xn[NF], t[NF];
+#pragma unroll
+  for (int q = 0; q < NF; ++q) xn[q] = R(0);
+  for (int st = 0; st <= N; ++st) {
+    issue(st + DEPTH - 1);
+    cp_async_wait<DEPTH - 1>();   // step st's group has landed
+    const int i = N - 1 - st;
+    const int stage = st % DEPTH;
+    R VC[DIM][NB], yu[B];
+    if (i + 1 < N) {
+#pragma unroll
+      for (int a = 0; a < DIM; ++a)
+#pragma unroll
+        for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(stage, BD::V_VC + a * NB + sl);
+#pragma unroll
+      for (int q = 0; q < B; ++q) yu[q] = *slot(stage, BD::V_Y + q);
+      mdot(VC, xn, t);
+    }
+    if (i < 0) {
+      R zero[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) zero[q] = R(0);
+      u_delta(0, yu, zero, t);   // dv_0 = 0 (pinned / frozen halo)
+      break;
+    }
+    R xb[B];
+#pragma unroll
+    for (int r = 0; r < B; ++r) xb[r] = *slot(stage, BD::V_B + r);
+    if (i + 1 < N) {
+      R T[B][B], dinv[B];
+#pragma unroll
+      for (int r = 1; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < r; ++c) T[r][c] = *slot(stage, BD::V_T + r * (r - 1) / 2 + c);
+#pragma unroll
+      for (int r = 0; r < B; ++r) dinv[r] = *slot(stage, BD::V_D + r);
+      R wf[NF], w[B];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) wf[q] = t[q];
+      lc.projP(wf);
+#pragma unroll
+      for (int q = 0; q < NF; ++q) w[q] = -wf[q] * idt;
+      w[NF] = R(0);
+      ldlt_solve<R, B>(T, dinv, w);   // K'^-1 w
+#pragma unroll
+      for (int r = 0; r < B; ++r) xb[r] -= w[r];
+    }
+    R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
+#pragma unroll
+    for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
+    if (i + 1 < N) {
+      R dvi[NF];
+#pragma unroll
+      for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
+      u_delta(i + 1, yu, dvi, t);
+    }
+#pragma unroll
+    for (int q = 0; q < NF; ++q) xn[q] = xb[q];
+  }
+  cp_async_wait<0>();
+}
+
 // x += omega * dx on the colour's unknowns (disjoint across cells)
 // x += omega * dx on the colour's unknowns (disjoint across cells); the
 // cell's face / cell offsets are computed once, FPT frames (blockIdx.z +
@@ -1203,6 +1364,8 @@ struct Nso : NsoBase {
   // backward: colours with >= back_flat cells use the unpipelined variant
   // (occupancy), smaller ones the load-pipelined one.  SMK_BACK_FLAT overrides.
   int64_t back_flat = 148 * 128 * 4;
+  // colours below 148*64 cells: cp.async-ring backward (SMK_BACK_DEEP=0 off)
+  bool back_deep = getenv("SMK_BACK_DEEP") == nullptr || atoi(getenv("SMK_BACK_DEEP")) != 0;
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
     if (const char* e = getenv("SMK_BACK_FLAT")) back_flat = atoll(e);
@@ -1451,6 +1614,15 @@ struct Nso : NsoBase {
       } else if (M >= back_flat) {
         k_scgs_back<DIM, PER, R, false, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
                                                                      (R)prm.omega, scratch, xout);
+      } else if (back_deep && M < 148 * 64) {
+        const size_t shm = (size_t)back_depth<R>() * BackDeep<DIM>::NV * 32 * sizeof(R);
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_scgs_back_deep<DIM, PER, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+          attr = true;
+        }
+        k_scgs_back_deep<DIM, PER, R><<<(unsigned)((M + 31) / 32), 32, shm, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
+                                                                                  mm[2], (R)prm.omega, scratch, xout);
       } else {
         k_scgs_back<DIM, PER, R, true, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
                                                                     (R)prm.omega, scratch, xout);

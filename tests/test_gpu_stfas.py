@@ -163,17 +163,23 @@ SHAPES = {"tm64p1": "0,0", "tm32p2": "1000000000,0", "tm32p4": "1000000000,10000
 
 @pytest.fixture
 def shape_env(monkeypatch):
-    def set_shape(fwd, back_flat):
+    def set_shape(fwd, back_flat, deep=1):
         monkeypatch.setenv("SMK_FWD_THRESH", SHAPES[fwd])
         monkeypatch.setenv("SMK_BACK_FLAT", str(back_flat))
+        monkeypatch.setenv("SMK_BACK_DEEP", str(deep))
     return set_shape
 
 
+# backward variants: unpipelined (back_flat 0), load-pipelined (deep off),
+# cp.async ring (deep on; the test colours are small)
+BACKS = {"flat": (0, 1), "pipe": (1 << 40, 0), "deep": (1 << 40, 1)}
+
+
 @pytest.mark.parametrize("fwd", list(SHAPES))
-@pytest.mark.parametrize("back_flat", [0, 1 << 40])
+@pytest.mark.parametrize("back", list(BACKS))
 @pytest.mark.parametrize("dim,bnd", [(2, "neumann"), (3, "neumann"), (3, "periodic")])
-def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back_flat, dim, bnd):
-    shape_env(fwd, back_flat)
+def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back, dim, bnd):
+    shape_env(fwd, *BACKS[back])
     pb = make_problem(dim, n=8, N=5, boundary=bnd, seed=23)
     rng = np.random.default_rng(7)
     st = random_state(pb, rng, 0.05)
