@@ -342,33 +342,48 @@ def main():
 
     # ---------------- end to end through the public API ----------------
     e2e = None
-    if not args.no_e2e and slab is None:
+    if not args.no_e2e:
+        # each rank: H2D of its inputs (its slab's state and level-0 guide --
+        # the whole problem at N = 1), the V-cycle, D2H of the updated state;
+        # device-timed, max over ranks
         pin = lambda t: t.detach().cpu().pin_memory()
-        h_vs = [pin(t) for t in vstar]
-        h_st = [pin(t) for t in (*state.V, state.PB, *state.U, state.P)]
+        if slab is None:
+            d_in = list(vstar) + [t for t in (*state.V, state.PB, *state.U, state.P)]
+        else:
+            d_in = list(slab.guides[0][0]) + [t for t in (*state.V, state.PB, *state.U, state.P)]
         d_st = [t for t in (*state.V, state.PB, *state.U, state.P)]
-        out_h = [torch.empty_like(t) for t in h_st]
-        out_h = [t.pin_memory() for t in out_h]
-        h2d = sum(t.numel() * t.element_size() for t in h_vs + h_st)
+        h_in = [pin(t) for t in d_in]
+        out_h = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_st]
+        h2d = sum(t.numel() * t.element_size() for t in h_in)
         d2h = sum(t.numel() * t.element_size() for t in out_h)
+        reps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         e_ms = 0.0
-        for _ in range(max(1, min(args.steps, 3))):
+        for _ in range(reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            for d, h in zip(vstar, h_vs):
+            for d, h in zip(d_in, h_in):
                 d.copy_(h, non_blocking=True)
-            for d, h in zip(d_st, h_st):
-                d.copy_(h, non_blocking=True)
-            hier.set_guide(v0, vstar)
+            if slab is None:
+                hier.set_guide(v0, vstar)
             step()
             for h, d in zip(out_h, d_st):
                 h.copy_(d, non_blocking=True)
             e1.record(stream)
             e1.synchronize()
             e_ms += e0.elapsed_time(e1)
-        e_ms /= max(1, min(args.steps, 3))
-        e2e = {"value": w.cell_timesteps * world / (e_ms / 1000.0), "unit": "cell-updates/s",
+        e_ms /= reps
+        if world > 1:
+            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+            hb = torch.tensor([float(h2d), float(d2h)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(hb, op=dist.ReduceOp.SUM)
+            h2d, d2h = hb[0].item(), hb[1].item()
+        e2e = {"value": w.cell_timesteps / (e_ms / 1000.0), "unit": "cell-updates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms}
 
     cpu = None
