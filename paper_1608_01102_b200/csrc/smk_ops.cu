@@ -272,89 +272,93 @@ __device__ __forceinline__ void pro_idx(int I, int n, int& i0, int& i1) {
 // Launch: x over the last (contiguous) axis, y over the rows of the leading
 // axes, z over frames -- the leading-axis coarse rows are block-uniform, so a
 // thread does only its own last-axis weights and 2^d coalesced loads.
-// Prolongation launch shape (cells and faces): one block per kProlongRows fine
-// rows of the leading axes (y) and frame (z); the block stages the 2^(d-1) coarse rows its
-// row interpolates from in shared memory, then every thread builds fine
-// elements along the contiguous axis from them.
-constexpr int kProlongRows = 8;
+// Prolongation launch shape (cells and faces): one warp per fine row of the
+// leading axes, 4 rows per 128-thread block (y), frame (z).  The warp issues
+// the row's old values (accumulate) and stages the 2^(d-1) coarse rows it
+// interpolates from in shared memory, then each lane builds fine elements
+// Fl = lane, lane + 32, ... along the contiguous axis: the row's index math
+// is done once per warp-row, not once per element, and only __syncwarp is
+// needed.
+constexpr int kProlongWarps = 4;
+constexpr int kProlongPerLane = 9;   // fine elements per lane with prefetched old values (nl <= 288)
 
 template <int DIM, bool PER, class R>
-__global__ void k_prolong_cell(Ix<DIM, PER> cx, Ix<DIM, PER> fx, const R* __restrict__ x, R* __restrict__ out,
-                               int N, int accumulate) {
+__global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_cell(Ix<DIM, PER> cx, Ix<DIM, PER> fx,
+                                                                    const R* __restrict__ x, R* __restrict__ out,
+                                                                    int N, int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* crow = reinterpret_cast<R*>(smem_raw);         // [2^(d-1)][cnl]
   constexpr int NR = DIM == 3 ? 4 : 2;
+  const int nl = DIM == 3 ? fx.n2 : fx.n1, cnl = DIM == 3 ? cx.n2 : cx.n1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * NR * cnl;   // this warp's [NR][cnl]
   const int64_t ncc = cx.cells(), ncf = fx.cells();
   const int fr = blockIdx.z;
-  const int nl = DIM == 3 ? fx.n2 : fx.n1, cnl = DIM == 3 ? cx.n2 : cx.n1;
   const int nrows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
+  const int row = blockIdx.y * kProlongWarps + warp;
+  if (row >= nrows) return;
   const R* p = x + (int64_t)fr * ncc;
-  const int rend = min(nrows, (int)(blockIdx.y + 1) * kProlongRows);
-  for (int row = blockIdx.y * kProlongRows; row < rend; ++row) {
-    const int F0 = DIM == 3 ? row / fx.n1 : row;
-    const int F1 = DIM == 3 ? row - F0 * fx.n1 : 0;
-    int a0, a1, b0 = 0, b1 = 0;
-    pro_idx<PER>(F0, cx.n0, a0, a1);
-    if (DIM == 3) pro_idx<PER>(F1, cx.n1, b0, b1);
-    R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? ((int64_t)F0 * fx.n1 + F1) * fx.n2 : (int64_t)F0 * fx.n1);
-    // the fine row's old values (accumulate) load alongside the coarse rows
-    R old[2] = {R(0), R(0)};
-    if (accumulate) {
+  const int F0 = DIM == 3 ? row / fx.n1 : row;
+  const int F1 = DIM == 3 ? row - F0 * fx.n1 : 0;
+  R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? ((int64_t)F0 * fx.n1 + F1) * fx.n2 : (int64_t)F0 * fx.n1);
+  R old[kProlongPerLane];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int Fl = threadIdx.x + u * blockDim.x;
-        if (Fl < nl) old[u] = orow[Fl];
-      }
-    }
-    __syncthreads();   // previous row's readers are done with crow
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? a1 : a0;
-      const int b = DIM == 3 ? ((r & 1) ? b1 : b0) : 0;
-      const R* src = p + (DIM == 3 ? cx.cell_off(a, b, 0) : cx.cell_off(a, 0, 0));
-      for (int l = threadIdx.x; l < cnl; l += blockDim.x) crow[r * cnl + l] = src[l];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int Fl = threadIdx.x + u * blockDim.x;
-      if (Fl >= nl) break;
-      int e0, e1;
-      pro_idx<PER>(Fl, cnl, e0, e1);
-      R res;
-      if (DIM == 3) {
-        // rows: 0 (a0,b0) 1 (a0,b1) 2 (a1,b0) 3 (a1,b1); axis 0, then 1, then 2
-        R y[2][2];
-        const int el[2] = {e0, e1};
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            y[b][e] = R(0.75) * crow[(0 * 2 + b) * cnl + el[e]] + R(0.25) * crow[(1 * 2 + b) * cnl + el[e]];
-        R z0 = R(0.75) * y[0][0] + R(0.25) * y[1][0];
-        R z1 = R(0.75) * y[0][1] + R(0.25) * y[1][1];
-        res = R(0.75) * z0 + R(0.25) * z1;
-      } else {
-        // rows: 0 (a0) 1 (a1); axis 0 then axis 1
-        R y0 = R(0.75) * crow[e0] + R(0.25) * crow[cnl + e0];
-        R y1 = R(0.75) * crow[e1] + R(0.25) * crow[cnl + e1];
-        res = R(0.75) * y0 + R(0.25) * y1;
-      }
-      orow[Fl] = accumulate ? old[u] + res : res;
-    }
+  for (int u = 0; u < kProlongPerLane; ++u) {
+    const int Fl = lane + 32 * u;
+    old[u] = (accumulate && Fl < nl) ? orow[Fl] : R(0);
   }
+  int a0, a1, b0 = 0, b1 = 0;
+  pro_idx<PER>(F0, cx.n0, a0, a1);
+  if (DIM == 3) pro_idx<PER>(F1, cx.n1, b0, b1);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? a1 : a0;
+    const int b = DIM == 3 ? ((r & 1) ? b1 : b0) : 0;
+    const R* src = p + (DIM == 3 ? cx.cell_off(a, b, 0) : cx.cell_off(a, 0, 0));
+    for (int l = lane; l < cnl; l += 32) crow[r * cnl + l] = src[l];
+  }
+  __syncwarp();
+  auto elem = [&](int Fl, R oldv) {
+    int e0, e1;
+    pro_idx<PER>(Fl, cnl, e0, e1);
+    R res;
+    if (DIM == 3) {
+      // rows: 0 (a0,b0) 1 (a0,b1) 2 (a1,b0) 3 (a1,b1); axis 0, then 1, then 2
+      R y[2][2];
+      const int el[2] = {e0, e1};
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          y[b][e] = R(0.75) * crow[(0 * 2 + b) * cnl + el[e]] + R(0.25) * crow[(1 * 2 + b) * cnl + el[e]];
+      R z0 = R(0.75) * y[0][0] + R(0.25) * y[1][0];
+      R z1 = R(0.75) * y[0][1] + R(0.25) * y[1][1];
+      res = R(0.75) * z0 + R(0.25) * z1;
+    } else {
+      // rows: 0 (a0) 1 (a1); axis 0 then axis 1
+      R y0 = R(0.75) * crow[e0] + R(0.25) * crow[cnl + e0];
+      R y1 = R(0.75) * crow[e1] + R(0.25) * crow[cnl + e1];
+      res = R(0.75) * y0 + R(0.25) * y1;
+    }
+    orow[Fl] = accumulate ? oldv + res : res;
+  };
+#pragma unroll
+  for (int u = 0; u < kProlongPerLane; ++u) {
+    const int Fl = lane + 32 * u;
+    if (Fl >= nl) break;
+    elem(Fl, old[u]);
+  }
+  for (int Fl = lane + 32 * kProlongPerLane; Fl < nl; Fl += 32) elem(Fl, accumulate ? orow[Fl] : R(0));
 }
 
 template <int DIM, bool PER>
 inline dim3 prolong_cell_grid(const Ix<DIM, PER>& fx, int N, int& tpb) {
-  const int nl = DIM == 3 ? fx.n2 : fx.n1;
-  tpb = nl >= 256 ? 256 : (nl + 31) / 32 * 32;   // <= 2 elements per thread
+  tpb = 32 * kProlongWarps;
   const int rows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
-  return dim3(1, (rows + kProlongRows - 1) / kProlongRows, N);
+  return dim3(1, (rows + kProlongWarps - 1) / kProlongWarps, N);
 }
 template <int DIM, bool PER, class R>
 inline size_t prolong_cell_smem(const Ix<DIM, PER>& cx) {
-  return (size_t)(DIM == 3 ? 4 : 2) * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
+  return (size_t)kProlongWarps * (DIM == 3 ? 4 : 2) * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
 }
 
 // face restriction: along the normal take the coincident (even) face, across
@@ -422,80 +426,81 @@ __device__ __forceinline__ void pro_face_axis(int I, int n_c_axis, bool normal, 
 
 // launch shape as k_prolong_cell, one launch per component k
 template <int DIM, bool PER, class R>
-__global__ void k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, int k, const R* __restrict__ in, R* __restrict__ out,
-                               int N, int accumulate) {
+__global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, int k,
+                                                                    const R* __restrict__ in, R* __restrict__ out,
+                                                                    int N, int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* crow = reinterpret_cast<R*>(smem_raw);         // [2^(d-1)][cnl]
   constexpr int NR = DIM == 3 ? 4 : 2;
-  const int64_t nfc = cx.faces(k), nff = fx.faces(k);
   const int L = DIM - 1;                             // last (contiguous) axis
   const int nl = fx.fe(k, L), cnl = cx.fe(k, L);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * NR * cnl;   // this warp's [NR][cnl]
+  const int64_t nfc = cx.faces(k), nff = fx.faces(k);
   const int fr = blockIdx.z;
   const int nrows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
+  const int row = blockIdx.y * kProlongWarps + warp;
+  if (row >= nrows) return;
   const R* p = in + (int64_t)fr * nfc;
-  const int rend = min(nrows, (int)(blockIdx.y + 1) * kProlongRows);
-  for (int row = blockIdx.y * kProlongRows; row < rend; ++row) {
-    int F[3] = {0, 0, 0};
-    if (DIM == 3) {
-      F[0] = row / fx.fe(k, 1);
-      F[1] = row - F[0] * fx.fe(k, 1);
-    } else {
-      F[0] = row;
-    }
-    int i0[3], i1[3];
-    R w0[3], w1[3];
-#pragma unroll
-    for (int a = 0; a < DIM - 1; ++a) pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
-    R* orow = out + (int64_t)fr * nff + fx.face_off(k, F[0], F[1], 0);
-    // the fine row's old values (accumulate) load alongside the coarse rows
-    R old[2] = {R(0), R(0)};
-    if (accumulate) {
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int Fl = threadIdx.x + u * blockDim.x;
-        if (Fl < nl) old[u] = orow[Fl];
-      }
-    }
-    __syncthreads();   // previous row's readers are done with crow
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? i1[0] : i0[0];
-      const int b = DIM == 3 ? ((r & 1) ? i1[1] : i0[1]) : 0;
-      const R* src = p + cx.face_off(k, a, b, 0);
-      for (int l = threadIdx.x; l < cnl; l += blockDim.x) crow[r * cnl + l] = src[l];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int Fl = threadIdx.x + u * blockDim.x;
-      if (Fl >= nl) break;
-      int il0, il1;
-      R wl0, wl1;
-      pro_face_axis<DIM, PER, R>(Fl, cx.n(L), L == k, il0, il1, wl0, wl1);
-      // sequential axis application: y over axis 0, then axis 1, then axis 2.
-      // A weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit.
-      // Rows: (axis-0 pick, axis-1 pick) -> index a * 2 + b (3D) / a (2D).
-      auto ax0 = [&](int b, int l) -> R {
-        R a = crow[(DIM == 3 ? 0 * 2 + b : 0) * cnl + l];
-        if (w1[0] == R(0)) return a;
-        return w0[0] * a + w1[0] * crow[(DIM == 3 ? 1 * 2 + b : 1) * cnl + l];
-      };
-      R res;
-      if (DIM == 3) {
-        auto ax1 = [&](int l) -> R {
-          R a = ax0(0, l);
-          if (w1[1] == R(0)) return a;
-          return w0[1] * a + w1[1] * ax0(1, l);
-        };
-        res = ax1(il0);
-        if (wl1 != R(0)) res = wl0 * res + wl1 * ax1(il1);
-      } else {
-        res = ax0(0, il0);
-        if (wl1 != R(0)) res = wl0 * res + wl1 * ax0(0, il1);
-      }
-      orow[Fl] = accumulate ? old[u] + res : res;
-    }
+  int F[3] = {0, 0, 0};
+  if (DIM == 3) {
+    F[0] = row / fx.fe(k, 1);
+    F[1] = row - F[0] * fx.fe(k, 1);
+  } else {
+    F[0] = row;
   }
+  R* orow = out + (int64_t)fr * nff + fx.face_off(k, F[0], F[1], 0);
+  R old[kProlongPerLane];
+#pragma unroll
+  for (int u = 0; u < kProlongPerLane; ++u) {
+    const int Fl = lane + 32 * u;
+    old[u] = (accumulate && Fl < nl) ? orow[Fl] : R(0);
+  }
+  int i0[3], i1[3];
+  R w0[3], w1[3];
+#pragma unroll
+  for (int a = 0; a < DIM - 1; ++a) pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? i1[0] : i0[0];
+    const int b = DIM == 3 ? ((r & 1) ? i1[1] : i0[1]) : 0;
+    const R* src = p + cx.face_off(k, a, b, 0);
+    for (int l = lane; l < cnl; l += 32) crow[r * cnl + l] = src[l];
+  }
+  __syncwarp();
+  auto elem = [&](int Fl, R oldv) {
+    int il0, il1;
+    R wl0, wl1;
+    pro_face_axis<DIM, PER, R>(Fl, cx.n(L), L == k, il0, il1, wl0, wl1);
+    // sequential axis application: y over axis 0, then axis 1, then axis 2.
+    // A weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit.
+    // Rows: (axis-0 pick, axis-1 pick) -> index a * 2 + b (3D) / a (2D).
+    auto ax0 = [&](int b, int l) -> R {
+      R a = crow[(DIM == 3 ? 0 * 2 + b : 0) * cnl + l];
+      if (w1[0] == R(0)) return a;
+      return w0[0] * a + w1[0] * crow[(DIM == 3 ? 1 * 2 + b : 1) * cnl + l];
+    };
+    R res;
+    if (DIM == 3) {
+      auto ax1 = [&](int l) -> R {
+        R a = ax0(0, l);
+        if (w1[1] == R(0)) return a;
+        return w0[1] * a + w1[1] * ax0(1, l);
+      };
+      res = ax1(il0);
+      if (wl1 != R(0)) res = wl0 * res + wl1 * ax1(il1);
+    } else {
+      res = ax0(0, il0);
+      if (wl1 != R(0)) res = wl0 * res + wl1 * ax0(0, il1);
+    }
+    orow[Fl] = accumulate ? oldv + res : res;
+  };
+#pragma unroll
+  for (int u = 0; u < kProlongPerLane; ++u) {
+    const int Fl = lane + 32 * u;
+    if (Fl >= nl) break;
+    elem(Fl, old[u]);
+  }
+  for (int Fl = lane + 32 * kProlongPerLane; Fl < nl; Fl += 32) elem(Fl, accumulate ? orow[Fl] : R(0));
 }
 
 // ===========================================================================
@@ -854,12 +859,12 @@ void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int ac
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
   for (int k = 0; k < DIM; ++k) {
-    const int nl = fx.fe(k, DIM - 1);
-    const int tpb = nl >= 256 ? 256 : (nl + 31) / 32 * 32;   // <= 2 elements per thread
     const int rows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
-    const dim3 grid(1, (rows + kProlongRows - 1) / kProlongRows, N);
-    const size_t shm = (size_t)(DIM == 3 ? 4 : 2) * cx.fe(k, DIM - 1) * sizeof(R);
-    k_prolong_face<DIM, PER, R><<<grid, tpb, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
+    const dim3 grid(1, (rows + kProlongWarps - 1) / kProlongWarps, N);
+    const size_t shm = (size_t)kProlongWarps * (DIM == 3 ? 4 : 2) * cx.fe(k, DIM - 1) * sizeof(R);
+    if (shm > 48 * 1024)
+      cudaFuncSetAttribute(k_prolong_face<DIM, PER, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    k_prolong_face<DIM, PER, R><<<grid, 32 * kProlongWarps, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
     count_launch();
   }
 }
