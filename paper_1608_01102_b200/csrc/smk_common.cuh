@@ -276,6 +276,20 @@ struct Loc {
     int o = of[2 * k] + d0 * fstride(ix, k, 0) + d1 * fstride(ix, k, 1) + (DIM == 3 ? d2 : 0);
     return v ? p + o : p;
   }
+  // address and in-range flag of the cell read at offset d (for async copies)
+  template <class R>
+  __device__ __forceinline__ const R* cell_ptr(const Ix<DIM, PER>& ix, const R* p, int d0, int d1, int d2,
+                                               bool& v) const {
+    if (PER) {
+      v = true;
+      int i = Ix<DIM, PER>::wrap(c[0] + d0, ix.n0), j = Ix<DIM, PER>::wrap(c[1] + d1, ix.n1);
+      int l = DIM == 3 ? Ix<DIM, PER>::wrap(c[2] + d2, ix.n2) : 0;
+      return p + ix.cell_off(i, j, l);
+    }
+    v = ok(0, d0, 1) && ok(1, d1, 1) && (DIM == 2 || ok(2, d2, 1));
+    int o = co + d0 * cstride(ix, 0) + d1 * cstride(ix, 1) + (DIM == 3 ? d2 : 0);
+    return v ? p + o : p;
+  }
   template <class R>
   __device__ __forceinline__ R cell(const Ix<DIM, PER>& ix, const R* __restrict__ p, int d0, int d1, int d2) const {
     if (PER) return ix.cell(p, c[0] + d0, c[1] + d1, c[2] + d2);

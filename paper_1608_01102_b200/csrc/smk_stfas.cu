@@ -83,6 +83,68 @@ struct KktCtx {
 // (the smoother assembles only unknown rows).  Same term order as
 // oracle/stfas.py kkt_residual; 1/h and 1/dt are multiplied, not divided.
 // ---------------------------------------------------------------------------
+// gathered scalar inputs of one pair's rows (besides the V / U caches)
+template <int DIM, class R>
+struct RowIn {
+  static constexpr int NF = 2 * DIM;
+  R pc, pbc;                  // P, PBAR at the cell
+  R pn[NF], pbn[NF];          // P, PBAR across each own face
+  R vsv[NF], unv[NF];         // guide v*_{i+1} and u_{i+1} at the own faces
+  R r1v[NF], r3v[NF], r2c, r4c;   // rhs rows (HR)
+};
+
+// the rows from the caches and the gathered inputs (no memory access)
+template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS, bool HR>
+__device__ __forceinline__ void rows_compute(const KktCtx<DIM, PER, R>& cx, const bool (&wall)[2 * DIM], bool inner,
+                                             const R (&VC)[DIM][NbrSlots<DIM>::NB],
+                                             const R (&UC)[DIM][NbrSlots<DIM>::NB], const R (&vp)[2 * DIM],
+                                             const RowIn<DIM, R>& g, R (&yu)[2 * DIM + 1], R (&yv)[2 * DIM + 1]) {
+  constexpr int NF = 2 * DIM;
+  static_for<NF>([&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    constexpr int j = q >> 1, sd = q & 1;
+    if constexpr (!BOTH && sd == 1) {
+      yu[q] = R(0);
+      yv[q] = R(0);
+    } else {
+      if (wall[q]) {
+        yu[q] = (WALLRHS && HR) ? R(0) - g.r3v[q] : R(0);
+        yv[q] = (WALLRHS && HR) ? R(0) - g.r1v[q] : R(0);
+      } else {
+        const R gp = sd ? (g.pn[q] - g.pc) * cx.ih : (g.pc - g.pn[q]) * cx.ih;
+        const R gpb = sd ? (g.pbn[q] - g.pbc) * cx.ih : (g.pbc - g.pbn[q]) * cx.ih;
+        const R vf = VC[j][sd + 1], uf = UC[j][sd + 1];
+        const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC, VC, true, true);
+        R a = (((vf - vp[q]) * cx.idt + adv) - uf) + gp;
+        R t1 = R(0);
+        if (inner) t1 = cx.kr * (vf - g.vsv[q]) - g.unv[q] * cx.idt;
+        const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC, UC) - S_cached<DIM, j, sd, R>(cx.c0, VC, UC, true, true);
+        R b = ((t1 + uf * cx.idt) + jt) + gpb;
+        if (HR) {
+          a -= g.r3v[q];
+          b -= g.r1v[q];
+        }
+        yu[q] = a;
+        yv[q] = b;
+      }
+    }
+  });
+  R dv = R(0), du = R(0);
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    R a = (VC[k][2] - VC[k][1]) * cx.ih;
+    R b = (UC[k][2] - UC[k][1]) * cx.ih;
+    dv = (k == 0) ? a : dv + a;
+    du = (k == 0) ? b : du + b;
+  }
+  if (HR) {
+    du -= g.r4c;
+    dv -= g.r2c;
+  }
+  yu[NF] = du;
+  yv[NF] = dv;
+}
+
 template <int DIM, bool PER, class R, bool BOTH, bool WALLRHS, bool HR, class LocT>
 __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const LocT& L,
                                           const bool (&wall)[2 * DIM], int i,
@@ -99,70 +161,30 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
   const Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Face3<R>{};
   // gather every scalar input first, so all of the pair's loads are in
   // flight together (one memory latency per pair, not one per face)
-  const R pc = Pi[L.co], pbc = PBi[L.co];
-  R pn[NF], pbn[NF], vsv[NF], unv[NF], r1v[NF], r3v[NF];
+  RowIn<DIM, R> g;
+  g.pc = Pi[L.co];
+  g.pbc = PBi[L.co];
   static_for<NF>([&](auto qc) {
     constexpr int q = decltype(qc)::value;
     constexpr int j = q >> 1, sd = q & 1;
     constexpr int d = sd ? 1 : -1;
     const bool on = (BOTH || sd == 0);
     const int64_t oo = (int64_t)i * cx.nf[j] + L.of[q];
-    pn[q] = (on && !wall[q]) ? L.cell(ix, Pi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
-    pbn[q] = (on && !wall[q]) ? L.cell(ix, PBi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
-    vsv[q] = (on && inner && !wall[q]) ? Vs.c[j][L.of[q]] : R(0);
-    unv[q] = (on && inner && !wall[q]) ? Un.c[j][L.of[q]] : R(0);
-    r1v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R1[j][oo] : R(0);
-    r3v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R3[j][oo] : R(0);
+    g.pn[q] = (on && !wall[q]) ? L.cell(ix, Pi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
+    g.pbn[q] = (on && !wall[q]) ? L.cell(ix, PBi, j == 0 ? d : 0, j == 1 ? d : 0, j == 2 ? d : 0) : R(0);
+    g.vsv[q] = (on && inner && !wall[q]) ? Vs.c[j][L.of[q]] : R(0);
+    g.unv[q] = (on && inner && !wall[q]) ? Un.c[j][L.of[q]] : R(0);
+    g.r1v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R1[j][oo] : R(0);
+    g.r3v[q] = (on && HR && (WALLRHS || !wall[q])) ? rhs.R3[j][oo] : R(0);
   });
-  R r2c = R(0), r4c = R(0);
+  g.r2c = R(0);
+  g.r4c = R(0);
   if (HR) {
     const int64_t o = (int64_t)i * cx.nc + L.co;
-    r4c = rhs.R4[o];
-    r2c = rhs.R2[o];
+    g.r4c = rhs.R4[o];
+    g.r2c = rhs.R2[o];
   }
-  static_for<NF>([&](auto qc) {
-    constexpr int q = decltype(qc)::value;
-    constexpr int j = q >> 1, sd = q & 1;
-    if constexpr (!BOTH && sd == 1) {
-      yu[q] = R(0);
-      yv[q] = R(0);
-    } else {
-      if (wall[q]) {
-        yu[q] = (WALLRHS && HR) ? R(0) - r3v[q] : R(0);
-        yv[q] = (WALLRHS && HR) ? R(0) - r1v[q] : R(0);
-      } else {
-        const R gp = sd ? (pn[q] - pc) * cx.ih : (pc - pn[q]) * cx.ih;
-        const R gpb = sd ? (pbn[q] - pbc) * cx.ih : (pbc - pbn[q]) * cx.ih;
-        const R vf = VC[j][sd + 1], uf = UC[j][sd + 1];
-        const R adv = S_cached<DIM, j, sd, R>(cx.c0, VC, VC, true, true);
-        R a = (((vf - vp[q]) * cx.idt + adv) - uf) + gp;
-        R t1 = R(0);
-        if (inner) t1 = cx.kr * (vf - vsv[q]) - unv[q] * cx.idt;
-        const R jt = T_cached<DIM, j, sd, R>(cx.c0, VC, UC) - S_cached<DIM, j, sd, R>(cx.c0, VC, UC, true, true);
-        R b = ((t1 + uf * cx.idt) + jt) + gpb;
-        if (HR) {
-          a -= r3v[q];
-          b -= r1v[q];
-        }
-        yu[q] = a;
-        yv[q] = b;
-      }
-    }
-  });
-  R dv = R(0), du = R(0);
-#pragma unroll
-  for (int k = 0; k < DIM; ++k) {
-    R a = (VC[k][2] - VC[k][1]) * cx.ih;
-    R b = (UC[k][2] - UC[k][1]) * cx.ih;
-    dv = (k == 0) ? a : dv + a;
-    du = (k == 0) ? b : du + b;
-  }
-  if (HR) {
-    du -= r4c;
-    dv -= r2c;
-  }
-  yu[NF] = du;
-  yv[NF] = dv;
+  rows_compute<DIM, PER, R, BOTH, WALLRHS, HR>(cx, wall, inner, VC, UC, vp, g, yu, yv);
 }
 
 // Eq. 8 residual f(x) - rhs, one thread per (frame, cell): the cell's lower
