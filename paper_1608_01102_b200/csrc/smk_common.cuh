@@ -486,6 +486,30 @@ __device__ __forceinline__ void cp_async_elem(R* smem, const R* gmem, bool valid
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
 }
+// 16-byte copy (L2 only), both addresses 16-byte aligned
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+// N consecutive values from 16-byte aligned shared memory, 16 bytes per load
+template <class R, int N>
+__device__ __forceinline__ void lds_vec(const R* p, R (&o)[N]) {
+  if constexpr (sizeof(R) == 4) {
+    static_assert(N % 4 == 0, "lds_vec: N % 4");
+#pragma unroll
+    for (int k = 0; k < N / 4; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(p)[k];
+      o[4 * k] = v.x; o[4 * k + 1] = v.y; o[4 * k + 2] = v.z; o[4 * k + 3] = v.w;
+    }
+  } else {
+    static_assert(N % 2 == 0, "lds_vec: N % 2");
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+      const double2 v = reinterpret_cast<const double2*>(p)[k];
+      o[2 * k] = v.x; o[2 * k + 1] = v.y;
+    }
+  }
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int K>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }

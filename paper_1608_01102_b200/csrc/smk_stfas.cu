@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -493,6 +494,16 @@ struct Line {
   static constexpr int T0 = 0, B0 = NT, Y0 = NL + 2 * B;
   static constexpr int L0 = 0, D0 = NL, Z0 = NL + B;
   static constexpr int SE = NL + 3 * B;
+  // record hand-off (shape-2 colours with the cp.async-ring backward): RS
+  // values per (pair, cell) -- M_i (row-major, written by the pair's
+  // producer), yu_i (padded to 8), then the consumer's L, 1/d and z -- in
+  // 16-byte groups interleaved over the cells, [i][RS / VW][m][VW] with VW =
+  // 16 / sizeof(R): one 16-byte store / cp.async per group and thread, a
+  // coalesced 512 B per warp
+  static constexpr int NY = 8;
+  static constexpr int NLDZ = (NL + 2 * B + 3) & ~3;
+  static constexpr int R_M = 0, R_Y = NF * NF, R_L = NF * NF + NY, R_D = R_L + NL, R_Z = R_D + B;
+  static constexpr int RS = R_L + NLDZ;
   static constexpr int NV = DIM * NbrSlots<DIM>::NB;     // V stencil values behind M
   static constexpr int NE = 2 * B + NV;                  // ring entry: yu, yv, V stencil
   static constexpr int E_YU = 0, E_YV = B, E_VS = 2 * B;
@@ -501,6 +512,21 @@ struct Line {
   static constexpr int NEP = 2 * NF + 1 + NF * NF + NT;
   static constexpr int P_C = 0, P_XR = NF, P_YC = 2 * NF, P_PM = 2 * NF + 1, P_D = 2 * NF + 1 + NF * NF;
 };
+
+// record group g0.. of (pair i, cell m): N values, 16 bytes per store
+template <class R, int N>
+__device__ __forceinline__ void stg_rec(R* scratch, int64_t M, int64_t m, int i, int rs, int e0, const R (&v)[N]) {
+  constexpr int VW = 16 / (int)sizeof(R);
+  static_assert(N % VW == 0, "stg_rec: N % VW");
+  R* p = scratch + (((int64_t)i * (rs / VW) + e0 / VW) * M + m) * VW;
+#pragma unroll
+  for (int k = 0; k < N / VW; ++k) {
+    if constexpr (sizeof(R) == 4)
+      *reinterpret_cast<float4*>(p + (int64_t)k * M * VW) = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    else
+      *reinterpret_cast<double2*>(p + (int64_t)k * M * VW) = make_double2(v[2 * k], v[2 * k + 1]);
+  }
+}
 
 // the consumer's dense inputs are built by the producers on the P = 4 shape
 __host__ __device__ constexpr bool fwd_prep(int P) { return P == 4; }
@@ -621,7 +647,8 @@ __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
   return esz == 8 ? (fwd_min_blocks_f32(TM, P) / 2 > 0 ? fwd_min_blocks_f32(TM, P) / 2 : 1) : fwd_min_blocks_f32(TM, P);
 }
 
-template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX, bool CMP>
+// FMT: hand-off format 0 factored, 1 compact (both [i][e][m]), 2 record
+template <int DIM, bool PER, class R, int TM, int P, bool HR, int NX, int FMT>
 __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R)))
     k_scgs_fwd(KktCtx<DIM, PER, R> cx, ResP<R> rhs, int o0, int o1, int o2, int mod, int m0, int m1,
                int m2, R* __restrict__ scratch, int* flag) {
@@ -629,6 +656,8 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   using PA = PairAlg<DIM, PER, R>;
   constexpr int NF = LN::NF, B = LN::B, NB = NbrSlots<DIM>::NB;
   constexpr bool PREP = fwd_prep(P);
+  constexpr bool CMP = FMT == 1, REC = FMT == 2;
+  static_assert(!REC || PREP, "record hand-off needs the prep shape");
   constexpr int NE = fwd_ring_entry<DIM>(P);
   constexpr int S = ring_stages(P);
   constexpr int NT = 2 * TM;   // threads per named barrier: one producer group + the consumers
@@ -678,7 +707,21 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         for (int q = 0; q < B; ++q) {
           yu[q] = -yu[q];
           yv[q] = -yv[q];
-          *sc(i, LN::Y0 + q) = yu[q];
+          if constexpr (!REC) *sc(i, LN::Y0 + q) = yu[q];
+        }
+        if constexpr (REC) {
+          // M_i and yu_i for the backward's step of pair i - 1 (M from the
+          // same function and inputs the backward used to rebuild it from)
+          R Mx[NF][NF], mr[NF * NF], yr[LN::NY];
+          jac_cached<DIM, R>(c0, idt, VC, cg.wall, Mx);
+#pragma unroll
+          for (int a = 0; a < NF; ++a)
+#pragma unroll
+            for (int b = 0; b < NF; ++b) mr[a * NF + b] = Mx[a][b];
+#pragma unroll
+          for (int q = 0; q < LN::NY; ++q) yr[q] = q < B ? yu[q] : R(0);
+          stg_rec<R, NF * NF>(scratch, M, m, i, LN::RS, LN::R_M, mr);
+          stg_rec<R, LN::NY>(scratch, M, m, i, LN::RS, LN::R_Y, yr);
         }
         if (P == 1) {
 #pragma unroll
@@ -823,6 +866,22 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   };
   // factored hand-off (small colours): L, 1/d and z of pair i
   auto store_factors = [&](int i, const R (&dinv)[B], const R (&z)[B]) {
+    if constexpr (REC) {
+      R v[LN::NLDZ];
+#pragma unroll
+      for (int r = 1; r < B; ++r)
+#pragma unroll
+        for (int c = 0; c < r; ++c) v[r * (r - 1) / 2 + c] = T[r][c];
+#pragma unroll
+      for (int r = 0; r < B; ++r) {
+        v[LN::NL + r] = dinv[r];
+        v[LN::NL + B + r] = z[r];
+      }
+#pragma unroll
+      for (int e = LN::NL + 2 * B; e < LN::NLDZ; ++e) v[e] = R(0);
+      stg_rec<R, LN::NLDZ>(scratch, M, m, i, LN::RS, LN::R_L, v);
+      return;
+    }
 #pragma unroll
     for (int r = 1; r < B; ++r)
 #pragma unroll
@@ -906,7 +965,14 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
       // alpha = 0: D~ is singular along M^-1 g; the saddle is not -> pivot
       ok &= saddle_solve_pivot<R, B>(T, b, tinyv);
     }
-    if (!CMP && act) {
+    if (REC && act) {
+      R v[LN::NLDZ];   // only z is read for the last pair
+#pragma unroll
+      for (int e = 0; e < LN::NLDZ; ++e) v[e] = R(0);
+#pragma unroll
+      for (int r = 0; r < B; ++r) v[LN::NL + B + r] = b[r];
+      stg_rec<R, LN::NLDZ>(scratch, M, m, i, LN::RS, LN::R_L, v);
+    } else if (!CMP && act) {
 #pragma unroll
       for (int r = 0; r < B; ++r) *sc(i, LN::Z0 + r) = b[r];
     }
@@ -1072,89 +1138,51 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   }
 }
 
-// Back substitution for small, latency-bound colours (factored hand-off):
-// one warp per 32 cells, and every thread streams its steps' inputs -- the
-// stored factors, u-rows and V stencil, 78 values in 3D -- through a DEPTH-
-// stage shared-memory ring filled by cp.async, DEPTH-1 steps ahead of the
-// serial recursion (zero-filled out-of-domain stencil reads, like Loc::face).
-// Same arithmetic as k_scgs_back<..., PIPE, ..., factored>.
-template <int DIM>
-struct BackDeep {
-  static constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
-  static constexpr int NL = B * (B - 1) / 2;
-  static constexpr int V_T = 0, V_B = NL, V_D = NL + B, V_Y = NL + 2 * B, V_VC = NL + 3 * B;
-  static constexpr int NV = NL + 3 * B + DIM * NB;    // values per step
-};
+// record pitch in shared memory (values): 16-byte aligned, and 16-byte
+// loads of 8 consecutive lanes land in distinct bank quads
+template <class R>
+__host__ __device__ constexpr int rec_pitch(int rs) {
+  return sizeof(R) == 4 ? (rs % 8 == 4 ? rs : rs + 4) : rs + 2;
+}
 template <class R>
 __host__ __device__ constexpr int back_depth() { return sizeof(R) == 4 ? 4 : 2; }
 
+// Back substitution of a shape-2 colour from the record hand-off: step s
+// handles pair i = N - 1 - s; its record (L, 1/d, z of pair i; M_i, yu_i for
+// the next step) arrives by 16-byte cp.async, DEPTH - 1 steps ahead.  M and yu
+// of pair i + 1 are carried in registers from the previous step, so nothing
+// is gathered or rebuilt from the state.  Same arithmetic, in the same order,
+// as k_scgs_back.
 template <int DIM, bool PER, class R>
 __global__ void __launch_bounds__(32) k_scgs_back_deep(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod,
                                                        int m0, int m1, int m2, R omega,
                                                        const R* __restrict__ scratch, R* __restrict__ xout) {
   using LN = Line<DIM>;
-  using BD = BackDeep<DIM>;
-  constexpr int NF = LN::NF, B = LN::B, NB = BD::NB, NV = BD::NV;
+  constexpr int NF = LN::NF, B = LN::B, NL = LN::NL, RS = LN::RS, RP = rec_pitch<R>(RS);
   constexpr int DEPTH = back_depth<R>();
+  constexpr int VW = 16 / (int)sizeof(R);
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  R* ring = reinterpret_cast<R*>(smem_raw);   // [DEPTH][NV][32]
-  const auto& ix = cx.ix;
+  R* ring = reinterpret_cast<R*>(smem_raw);   // [DEPTH][32][RP]
   const int N = cx.N;
   const int64_t M = (int64_t)m0 * m1 * m2;
   const int lane = threadIdx.x;
   const int64_t m = (int64_t)blockIdx.x * 32 + lane;
   if (m >= M) return;   // no block-wide synchronisation below
-  const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
+  const LineCell<DIM, PER, R> lc(cx.ix, cx.h, m, o0, o1, o2, mod, m1, m2);
   const auto& cg = lc.cg;
-  const Loc<DIM, PER> L(ix, cg.c);
   const R idt = cx.idt;
-  auto gsc = [&](int i, int e) -> const R* { return scratch + ((int64_t)i * LN::SE + e) * M + m; };
-  auto slot = [&](int stage, int v) -> R* { return ring + (stage * NV + v) * 32 + lane; };
-  // step s handles pair i = N - 1 - s (s = N: only pair 0's u-block)
+  auto stage = [&](int st) -> R* { return ring + ((st % DEPTH) * 32 + lane) * RP; };
   auto issue = [&](int st) {
     const int i = N - 1 - st;
-    if (i >= -1) {
-      const int stage = st % DEPTH;
-      if (i >= 0) {
-        if (i + 1 < N) {
+    if (i >= 0) {
+      const R* src = scratch + ((int64_t)i * (RS / VW) * M + m) * VW;
+      R* dst = stage(st);
 #pragma unroll
-          for (int e = 0; e < BD::NL; ++e) cp_async_elem(slot(stage, BD::V_T + e), gsc(i, LN::L0 + e), true);
-#pragma unroll
-          for (int r = 0; r < B; ++r) cp_async_elem(slot(stage, BD::V_D + r), gsc(i, LN::D0 + r), true);
-        }
-#pragma unroll
-        for (int r = 0; r < B; ++r) cp_async_elem(slot(stage, BD::V_B + r), gsc(i, LN::Z0 + r), true);
-      }
-      if (i + 1 < N) {
-#pragma unroll
-        for (int q = 0; q < B; ++q) cp_async_elem(slot(stage, BD::V_Y + q), gsc(i + 1, LN::Y0 + q), true);
-        const Face3<R> Vf = frame_of(cx.V, i + 1, cx.nf);
-#pragma unroll
-        for (int a = 0; a < DIM; ++a)
-#pragma unroll
-          for (int sl = 0; sl < NB; ++sl) {
-            int d[3];
-            NbrSlots<DIM>::offset(a, sl, d);
-            bool v;
-            const R* src = L.face_ptr(ix, Vf.c[a], a, d[0], d[1], d[2], v);
-            cp_async_elem(slot(stage, BD::V_VC + a * NB + sl), src, v);
-          }
-      }
+      for (int k = 0; k < RS / VW; ++k) cp_async16(dst + k * VW, src + (int64_t)k * M * VW);
     }
     cp_async_commit();   // one group per step (empty past the end)
   };
-  auto mdot = [&](const R (&VC)[DIM][NB], const R (&dv)[NF], R (&t)[NF]) {
-    R Mi[NF][NF];
-    jac_cached<DIM, R>(cx.c0, idt, VC, cg.wall, Mi);
-#pragma unroll
-    for (int q = 0; q < NF; ++q) {
-      R s = R(0);
-#pragma unroll
-      for (int k = 0; k < NF; ++k) s += Mi[q][k] * dv[k];
-      t[q] = s;
-    }
-  };
-  auto u_delta = [&](int ip, const R (&yu)[B], const R (&dvi)[NF], const R (&t)[NF]) {
+  auto u_delta = [&](int ip, const R (&yu)[LN::NY], const R (&dvi)[NF], const R (&t)[NF]) {
     R a[NF];
     R ga = R(0);
 #pragma unroll
@@ -1171,42 +1199,44 @@ __global__ void __launch_bounds__(32) k_scgs_back_deep(KktCtx<DIM, PER, R> cx, i
   };
 #pragma unroll
   for (int st = 0; st < DEPTH - 1; ++st) issue(st);
-  R xn[NF], t[NF];
+  R xn[NF], Mn[NF * NF], yun[LN::NY];   // dv, M and yu of pair i + 1
 #pragma unroll
   for (int q = 0; q < NF; ++q) xn[q] = R(0);
   for (int st = 0; st <= N; ++st) {
     issue(st + DEPTH - 1);
-    cp_async_wait<DEPTH - 1>();   // step st's group has landed
+    cp_async_wait<DEPTH - 1>();   // step st's record has landed
     const int i = N - 1 - st;
-    const int stage = st % DEPTH;
-    R VC[DIM][NB], yu[B];
+    const R* cur = stage(st);
+    R t[NF];   // M_{i+1} dv_{i+1}
     if (i + 1 < N) {
 #pragma unroll
-      for (int a = 0; a < DIM; ++a)
+      for (int q = 0; q < NF; ++q) {
+        R s = R(0);
 #pragma unroll
-        for (int sl = 0; sl < NB; ++sl) VC[a][sl] = *slot(stage, BD::V_VC + a * NB + sl);
-#pragma unroll
-      for (int q = 0; q < B; ++q) yu[q] = *slot(stage, BD::V_Y + q);
-      mdot(VC, xn, t);
+        for (int k = 0; k < NF; ++k) s += Mn[q * NF + k] * xn[k];
+        t[q] = s;
+      }
     }
     if (i < 0) {
       R zero[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) zero[q] = R(0);
-      u_delta(0, yu, zero, t);   // dv_0 = 0 (pinned / frozen halo)
+      u_delta(0, yun, zero, t);   // dv_0 = 0 (pinned / frozen halo)
       break;
     }
+    R ldz[LN::NLDZ];
+    lds_vec<R, LN::NLDZ>(cur + LN::R_L, ldz);
     R xb[B];
 #pragma unroll
-    for (int r = 0; r < B; ++r) xb[r] = *slot(stage, BD::V_B + r);
+    for (int r = 0; r < B; ++r) xb[r] = ldz[NL + B + r];
     if (i + 1 < N) {
       R T[B][B], dinv[B];
 #pragma unroll
       for (int r = 1; r < B; ++r)
 #pragma unroll
-        for (int c = 0; c < r; ++c) T[r][c] = *slot(stage, BD::V_T + r * (r - 1) / 2 + c);
+        for (int c = 0; c < r; ++c) T[r][c] = ldz[r * (r - 1) / 2 + c];
 #pragma unroll
-      for (int r = 0; r < B; ++r) dinv[r] = *slot(stage, BD::V_D + r);
+      for (int r = 0; r < B; ++r) dinv[r] = ldz[NL + r];
       R wf[NF], w[B];
 #pragma unroll
       for (int q = 0; q < NF; ++q) wf[q] = t[q];
@@ -1225,10 +1255,13 @@ __global__ void __launch_bounds__(32) k_scgs_back_deep(KktCtx<DIM, PER, R> cx, i
       R dvi[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
-      u_delta(i + 1, yu, dvi, t);
+      u_delta(i + 1, yun, dvi, t);
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];
+    // pair i's M and yu, for step st + 1 (before the next issue reuses the stage)
+    lds_vec<R, NF * NF>(cur + LN::R_M, Mn);
+    lds_vec<R, LN::NY>(cur + LN::R_Y, yun);
   }
   cp_async_wait<0>();
 }
@@ -1434,7 +1467,11 @@ struct Nso : NsoBase {
       maxM = M > maxM ? M : maxM;
     }
     constexpr int B = Slots<DIM>::B;
-    scratch = alloc((int64_t)N * Line<DIM>::SE * maxM);
+    // [i][e][m] formats: SE values per pair; record format (shape-2 colours,
+    // fewer than fwd_mid cells): RS
+    const int64_t rec_m = back_deep ? (maxM < fwd_mid ? maxM : fwd_mid) : 0;
+    const int64_t per_pair = std::max((int64_t)Line<DIM>::SE * maxM, (int64_t)Line<DIM>::RS * rec_m);
+    scratch = alloc((int64_t)N * per_pair);
     xout = alloc((int64_t)2 * N * B * maxM);
     flag = (int*)mem.get(64);
     parts = (double*)mem.get(sizeof(double) * 70000);
@@ -1563,11 +1600,11 @@ struct Nso : NsoBase {
     f(std::integral_constant<int, 0>{});
   }
 
-  template <int TM, int P, bool HR, int NX, bool CMP>
+  template <int TM, int P, bool HR, int NX, int FMT>
   void launch_fwd_t(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, const int o[3], int mod, const int mm[3], int64_t M,
                     cudaStream_t st) {
     const size_t shm = (size_t)ring_stages(P) * fwd_ring_entry<DIM>(P) * TM * sizeof(R);
-    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX, CMP>;
+    auto kern = k_scgs_fwd<DIM, PER, R, TM, P, HR, NX, FMT>;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -1577,11 +1614,11 @@ struct Nso : NsoBase {
                                                                    scratch, flag);
     count_launch();
   }
-  template <int TM, int P, int NX, bool CMP>
+  template <int TM, int P, int NX, int FMT>
   void launch_fwd(const KktCtx<DIM, PER, R>& c, const ResP<R>& r, bool hr, const int o[3], int mod, const int mm[3],
                   int64_t M, cudaStream_t st) {
-    if (hr) launch_fwd_t<TM, P, true, NX, CMP>(c, r, o, mod, mm, M, st);
-    else launch_fwd_t<TM, P, false, NX, CMP>(c, r, o, mod, mm, M, st);
+    if (hr) launch_fwd_t<TM, P, true, NX, FMT>(c, r, o, mod, mm, M, st);
+    else launch_fwd_t<TM, P, false, NX, FMT>(c, r, o, mod, mm, M, st);
   }
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
@@ -1610,15 +1647,16 @@ struct Nso : NsoBase {
     // format, small latency-bound ones the factored format
     const bool cmp = M >= back_flat && shape == 0;
     if (shape == 2) {
-      launch_fwd<32, 4, 0, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
+      if (back_deep) launch_fwd<32, 4, 0, 2>(c, r, rhs != nullptr, o, mod, mm, M, st);
+      else launch_fwd<32, 4, 0, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
     } else {
       with_nx(l, [&](auto nxc) {
         constexpr int NXv = decltype(nxc)::value;
         if (shape == 0) {
-          if (cmp) launch_fwd<64, 1, NXv, true>(c, r, rhs != nullptr, o, mod, mm, M, st);
-          else launch_fwd<64, 1, NXv, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
+          if (cmp) launch_fwd<64, 1, NXv, 1>(c, r, rhs != nullptr, o, mod, mm, M, st);
+          else launch_fwd<64, 1, NXv, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
         } else {
-          launch_fwd<32, 2, NXv, false>(c, r, rhs != nullptr, o, mod, mm, M, st);
+          launch_fwd<32, 2, NXv, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
         }
       });
     }
@@ -1633,11 +1671,8 @@ struct Nso : NsoBase {
           k_scgs_back<DIM, PER, R, false, NXv, true><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
                                                                         mm[2], (R)prm.omega, scratch, xout);
         });
-      } else if (M >= back_flat) {
-        k_scgs_back<DIM, PER, R, false, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                                     (R)prm.omega, scratch, xout);
-      } else if (back_deep && M < 148 * 64) {
-        const size_t shm = (size_t)back_depth<R>() * BackDeep<DIM>::NV * 32 * sizeof(R);
+      } else if (shape == 2 && back_deep) {   // record hand-off
+        const size_t shm = (size_t)back_depth<R>() * 32 * rec_pitch<R>(Line<DIM>::RS) * sizeof(R);
         static bool attr = false;
         if (!attr) {
           cudaFuncSetAttribute(k_scgs_back_deep<DIM, PER, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -1645,6 +1680,9 @@ struct Nso : NsoBase {
         }
         k_scgs_back_deep<DIM, PER, R><<<(unsigned)((M + 31) / 32), 32, shm, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
                                                                                   mm[2], (R)prm.omega, scratch, xout);
+      } else if (M >= back_flat) {
+        k_scgs_back<DIM, PER, R, false, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
+                                                                     (R)prm.omega, scratch, xout);
       } else {
         k_scgs_back<DIM, PER, R, true, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
                                                                     (R)prm.omega, scratch, xout);
