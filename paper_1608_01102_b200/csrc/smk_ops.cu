@@ -274,23 +274,87 @@ __device__ __forceinline__ void pro_idx(int I, int n, int& i0, int& i1) {
 // thread does only its own last-axis weights and 2^d coalesced loads.
 // Prolongation launch shape (cells and faces): one warp per fine row of the
 // leading axes, 4 rows per 128-thread block (y), frame (z).  The warp issues
-// the row's old values (accumulate) and stages the 2^(d-1) coarse rows it
-// interpolates from in shared memory, then each lane builds fine elements
-// Fl = lane, lane + 32, ... along the contiguous axis: the row's index math
-// is done once per warp-row, not once per element, and only __syncwarp is
-// needed.
+// the row's old values (accumulate) and the 2^(d-1) coarse rows it
+// interpolates from, combines the coarse rows across the leading axes ONCE
+// per coarse element into one shared-memory row c (the same expressions, in
+// the same axis order, as per fine element), then each lane builds the fine
+// pair (2j, 2j+1) along the contiguous axis from c[j-1..j+1]: a few
+// instructions per fine element (the per-element leading-axis work made the
+// first version issue-bound at 1.6 TB/s).
 constexpr int kProlongWarps = 4;
-constexpr int kProlongPerLane = 9;   // fine elements per lane with prefetched old values (nl <= 288)
+// fine pairs per lane with prefetched old values: MAXP = 3 (nl <= 192) or 5
+// (nl <= 320, longer rows finish in a tail loop), chosen per launch
 
-template <int DIM, bool PER, class R>
+
+// fine pair (2j, 2j+1) of a row from the combined coarse row c (cn values):
+// normal: 2j copies c[j], 2j+1 averages c[j], c[j+1]; across: (3/4, 1/4)
+// with c[j-1] / c[j+1] (clamped, or wrapped when periodic)
+template <bool PER, class R>
+__device__ __forceinline__ void pro_pair(const R* c, int j, int cn, bool normal, R& f0, R& f1) {
+  const R cj = c[j];
+  if (normal) {
+    int jn = j + 1;
+    if (PER && jn >= cn) jn -= cn;
+    if (!PER && jn > cn - 1) jn = cn - 1;   // only reached past the row end
+    f0 = cj;
+    f1 = R(0.5) * cj + R(0.5) * c[jn];
+  } else {
+    int jm = j - 1, jp = j + 1;
+    if (PER) {
+      jm = jm < 0 ? jm + cn : jm;
+      jp = jp >= cn ? jp - cn : jp;
+    } else {
+      jm = jm < 0 ? 0 : jm;
+      jp = jp > cn - 1 ? cn - 1 : jp;
+    }
+    f0 = R(0.75) * cj + R(0.25) * c[jm];
+    f1 = R(0.75) * cj + R(0.25) * c[jp];
+  }
+}
+
+// old values of the fine row (issued before the coarse loads)
+template <class R, int MAXP>
+__device__ __forceinline__ void pro_old(const R* orow, int nl, int lane, int accumulate, R (&old)[MAXP][2]) {
+#pragma unroll
+  for (int u = 0; u < MAXP; ++u) {
+    const int F = 2 * (lane + 32 * u);
+    old[u][0] = (accumulate && F < nl) ? orow[F] : R(0);
+    old[u][1] = (accumulate && F + 1 < nl) ? orow[F + 1] : R(0);
+  }
+}
+// fine row phase shared by cells and faces: orow[0..nl) (+)= pairs from c
+template <bool PER, class R, int MAXP>
+__device__ __forceinline__ void pro_row(const R* c, int cn, bool normal, R* orow, int nl, int lane, int accumulate,
+                                        const R (&old)[MAXP][2]) {
+  const int np = (nl + 1) >> 1;
+  auto put = [&](int j, R o0, R o1) {
+    R f0, f1;
+    pro_pair<PER, R>(c, j, cn, normal, f0, f1);
+    const int F = 2 * j;
+    orow[F] = accumulate ? o0 + f0 : f0;
+    if (F + 1 < nl) orow[F + 1] = accumulate ? o1 + f1 : f1;
+  };
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < MAXP; ++u) {
+    const int j = lane + 32 * u;
+    if (j >= np) break;
+    put(j, old[u][0], old[u][1]);
+  }
+  for (int j = lane + 32 * MAXP; j < np; j += 32) {
+    const int F = 2 * j;
+    put(j, accumulate ? orow[F] : R(0), (accumulate && F + 1 < nl) ? orow[F + 1] : R(0));
+  }
+}
+
+template <int DIM, bool PER, class R, int MAXP>
 __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_cell(Ix<DIM, PER> cx, Ix<DIM, PER> fx,
                                                                     const R* __restrict__ x, R* __restrict__ out,
                                                                     int N, int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NR = DIM == 3 ? 4 : 2;
   const int nl = DIM == 3 ? fx.n2 : fx.n1, cnl = DIM == 3 ? cx.n2 : cx.n1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  R* crow = reinterpret_cast<R*>(smem_raw) + warp * NR * cnl;   // this warp's [NR][cnl]
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * cnl;   // this warp's combined coarse row
   const int64_t ncc = cx.cells(), ncf = fx.cells();
   const int fr = blockIdx.z;
   const int nrows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
@@ -299,55 +363,27 @@ __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_cell(Ix<DIM, PER
   const R* p = x + (int64_t)fr * ncc;
   const int F0 = DIM == 3 ? row / fx.n1 : row;
   const int F1 = DIM == 3 ? row - F0 * fx.n1 : 0;
-  R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? ((int64_t)F0 * fx.n1 + F1) * fx.n2 : (int64_t)F0 * fx.n1);
-  R old[kProlongPerLane];
-#pragma unroll
-  for (int u = 0; u < kProlongPerLane; ++u) {
-    const int Fl = lane + 32 * u;
-    old[u] = (accumulate && Fl < nl) ? orow[Fl] : R(0);
-  }
+  // in-frame offsets in 32 bits (a frame has < 2^31 elements)
+  R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? (F0 * fx.n1 + F1) * fx.n2 : F0 * fx.n1);
+  R old[MAXP][2];
+  pro_old<R, MAXP>(orow, nl, lane, accumulate, old);
   int a0, a1, b0 = 0, b1 = 0;
   pro_idx<PER>(F0, cx.n0, a0, a1);
   if (DIM == 3) pro_idx<PER>(F1, cx.n1, b0, b1);
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? a1 : a0;
-    const int b = DIM == 3 ? ((r & 1) ? b1 : b0) : 0;
-    const R* src = p + (DIM == 3 ? cx.cell_off(a, b, 0) : cx.cell_off(a, 0, 0));
-    for (int l = lane; l < cnl; l += 32) crow[r * cnl + l] = src[l];
-  }
-  __syncwarp();
-  auto elem = [&](int Fl, R oldv) {
-    int e0, e1;
-    pro_idx<PER>(Fl, cnl, e0, e1);
-    R res;
-    if (DIM == 3) {
-      // rows: 0 (a0,b0) 1 (a0,b1) 2 (a1,b0) 3 (a1,b1); axis 0, then 1, then 2
-      R y[2][2];
-      const int el[2] = {e0, e1};
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          y[b][e] = R(0.75) * crow[(0 * 2 + b) * cnl + el[e]] + R(0.25) * crow[(1 * 2 + b) * cnl + el[e]];
-      R z0 = R(0.75) * y[0][0] + R(0.25) * y[1][0];
-      R z1 = R(0.75) * y[0][1] + R(0.25) * y[1][1];
-      res = R(0.75) * z0 + R(0.25) * z1;
-    } else {
-      // rows: 0 (a0) 1 (a1); axis 0 then axis 1
-      R y0 = R(0.75) * crow[e0] + R(0.25) * crow[cnl + e0];
-      R y1 = R(0.75) * crow[e1] + R(0.25) * crow[cnl + e1];
-      res = R(0.75) * y0 + R(0.25) * y1;
+  if (DIM == 3) {
+    // axis 0 (a), then axis 1 (b): y_b = 3/4 (a0, b) + 1/4 (a1, b); c = 3/4 y_b0 + 1/4 y_b1
+    const R *r00 = p + (a0 * cx.n1 + b0) * cx.n2, *r01 = p + (a0 * cx.n1 + b1) * cx.n2;
+    const R *r10 = p + (a1 * cx.n1 + b0) * cx.n2, *r11 = p + (a1 * cx.n1 + b1) * cx.n2;
+    for (int l = lane; l < cnl; l += 32) {
+      const R y0 = R(0.75) * r00[l] + R(0.25) * r10[l];
+      const R y1 = R(0.75) * r01[l] + R(0.25) * r11[l];
+      crow[l] = R(0.75) * y0 + R(0.25) * y1;
     }
-    orow[Fl] = accumulate ? oldv + res : res;
-  };
-#pragma unroll
-  for (int u = 0; u < kProlongPerLane; ++u) {
-    const int Fl = lane + 32 * u;
-    if (Fl >= nl) break;
-    elem(Fl, old[u]);
+  } else {
+    const R *r0 = p + a0 * cx.n1, *r1 = p + a1 * cx.n1;
+    for (int l = lane; l < cnl; l += 32) crow[l] = R(0.75) * r0[l] + R(0.25) * r1[l];
   }
-  for (int Fl = lane + 32 * kProlongPerLane; Fl < nl; Fl += 32) elem(Fl, accumulate ? orow[Fl] : R(0));
+  pro_row<PER, R, MAXP>(crow, cnl, false, orow, nl, lane, accumulate, old);
 }
 
 template <int DIM, bool PER>
@@ -358,7 +394,7 @@ inline dim3 prolong_cell_grid(const Ix<DIM, PER>& fx, int N, int& tpb) {
 }
 template <int DIM, bool PER, class R>
 inline size_t prolong_cell_smem(const Ix<DIM, PER>& cx) {
-  return (size_t)kProlongWarps * (DIM == 3 ? 4 : 2) * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
+  return (size_t)kProlongWarps * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
 }
 
 // face restriction: along the normal take the coincident (even) face, across
@@ -425,16 +461,15 @@ __device__ __forceinline__ void pro_face_axis(int I, int n_c_axis, bool normal, 
 }
 
 // launch shape as k_prolong_cell, one launch per component k
-template <int DIM, bool PER, class R>
+template <int DIM, bool PER, class R, int MAXP>
 __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_face(Ix<DIM, PER> cx, Ix<DIM, PER> fx, int k,
                                                                     const R* __restrict__ in, R* __restrict__ out,
                                                                     int N, int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int NR = DIM == 3 ? 4 : 2;
   const int L = DIM - 1;                             // last (contiguous) axis
   const int nl = fx.fe(k, L), cnl = cx.fe(k, L);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  R* crow = reinterpret_cast<R*>(smem_raw) + warp * NR * cnl;   // this warp's [NR][cnl]
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * cnl;   // this warp's combined coarse row
   const int64_t nfc = cx.faces(k), nff = fx.faces(k);
   const int fr = blockIdx.z;
   const int nrows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
@@ -448,59 +483,35 @@ __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_face(Ix<DIM, PER
   } else {
     F[0] = row;
   }
-  R* orow = out + (int64_t)fr * nff + fx.face_off(k, F[0], F[1], 0);
-  R old[kProlongPerLane];
-#pragma unroll
-  for (int u = 0; u < kProlongPerLane; ++u) {
-    const int Fl = lane + 32 * u;
-    old[u] = (accumulate && Fl < nl) ? orow[Fl] : R(0);
-  }
-  int i0[3], i1[3];
-  R w0[3], w1[3];
+  const int fe1 = fx.fe(k, 1), fe2 = DIM == 3 ? fx.fe(k, 2) : 1;
+  const int ce1 = cx.fe(k, 1), ce2 = DIM == 3 ? cx.fe(k, 2) : 1;
+  // in-frame offsets in 32 bits (a frame has < 2^31 elements)
+  R* orow = out + (int64_t)fr * nff + (F[0] * fe1 + F[1]) * fe2;
+  R old[MAXP][2];
+  pro_old<R, MAXP>(orow, nl, lane, accumulate, old);
+  int i0[2] = {0, 0}, i1[2] = {0, 0};
+  R w0[2] = {R(1), R(1)}, w1[2] = {R(0), R(0)};
 #pragma unroll
   for (int a = 0; a < DIM - 1; ++a) pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
+  // sequential axis application over the leading axes (axis 0, then 1); a
+  // weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit
+  const R* rr[2][2];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int a = (r >> (DIM == 3 ? 1 : 0)) & 1 ? i1[0] : i0[0];
-    const int b = DIM == 3 ? ((r & 1) ? i1[1] : i0[1]) : 0;
-    const R* src = p + cx.face_off(k, a, b, 0);
-    for (int l = lane; l < cnl; l += 32) crow[r * cnl + l] = src[l];
-  }
-  __syncwarp();
-  auto elem = [&](int Fl, R oldv) {
-    int il0, il1;
-    R wl0, wl1;
-    pro_face_axis<DIM, PER, R>(Fl, cx.n(L), L == k, il0, il1, wl0, wl1);
-    // sequential axis application: y over axis 0, then axis 1, then axis 2.
-    // A weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit.
-    // Rows: (axis-0 pick, axis-1 pick) -> index a * 2 + b (3D) / a (2D).
-    auto ax0 = [&](int b, int l) -> R {
-      R a = crow[(DIM == 3 ? 0 * 2 + b : 0) * cnl + l];
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+      rr[x][y] = p + ((x ? i1[0] : i0[0]) * ce1 + (DIM == 3 ? (y ? i1[1] : i0[1]) : 0)) * ce2;
+  for (int l = lane; l < cnl; l += 32) {
+    auto ax0 = [&](int y) -> R {
+      const R a = rr[0][y][l];
       if (w1[0] == R(0)) return a;
-      return w0[0] * a + w1[0] * crow[(DIM == 3 ? 1 * 2 + b : 1) * cnl + l];
+      return w0[0] * a + w1[0] * rr[1][y][l];
     };
-    R res;
-    if (DIM == 3) {
-      auto ax1 = [&](int l) -> R {
-        R a = ax0(0, l);
-        if (w1[1] == R(0)) return a;
-        return w0[1] * a + w1[1] * ax0(1, l);
-      };
-      res = ax1(il0);
-      if (wl1 != R(0)) res = wl0 * res + wl1 * ax1(il1);
-    } else {
-      res = ax0(0, il0);
-      if (wl1 != R(0)) res = wl0 * res + wl1 * ax0(0, il1);
-    }
-    orow[Fl] = accumulate ? oldv + res : res;
-  };
-#pragma unroll
-  for (int u = 0; u < kProlongPerLane; ++u) {
-    const int Fl = lane + 32 * u;
-    if (Fl >= nl) break;
-    elem(Fl, old[u]);
+    R c = ax0(0);
+    if (DIM == 3 && w1[1] != R(0)) c = w0[1] * c + w1[1] * ax0(1);
+    crow[l] = c;
   }
-  for (int Fl = lane + 32 * kProlongPerLane; Fl < nl; Fl += 32) elem(Fl, accumulate ? orow[Fl] : R(0));
+  pro_row<PER, R, MAXP>(crow, cnl, L == k, orow, nl, lane, accumulate, old);
 }
 
 // ===========================================================================
@@ -839,13 +850,21 @@ void launch_restrict_cell(const Geo& gf, int N, const R* x, R* out, cudaStream_t
   k_restrict_cell<DIM, PER, R><<<frame_grid(cx.cells(), N, 256), 256, 0, st>>>(fx, cx, x, out, N); count_launch();
 }
 template <int DIM, bool PER, class R>
+void prolong_cell_go(const Ix<DIM, PER>& cx, const Ix<DIM, PER>& fx, int N, const R* x, R* out, int acc,
+                     cudaStream_t st) {
+  int tpb;
+  const dim3 grid = prolong_cell_grid(fx, N, tpb);
+  const size_t shm = prolong_cell_smem<DIM, PER, R>(cx);
+  const int nl = DIM == 3 ? fx.n2 : fx.n1;
+  if (nl <= 192) k_prolong_cell<DIM, PER, R, 3><<<grid, tpb, shm, st>>>(cx, fx, x, out, N, acc);
+  else k_prolong_cell<DIM, PER, R, 5><<<grid, tpb, shm, st>>>(cx, fx, x, out, N, acc);
+  count_launch();
+}
+template <int DIM, bool PER, class R>
 void launch_prolong_cell(const Geo& gc, int N, const R* x, R* out, int acc, cudaStream_t st) {
   Geo gf = refine(gc);
   Ix<DIM, PER> fx(gf), cx(gc);
-  int tpb;
-  const dim3 grid = prolong_cell_grid(fx, N, tpb);
-  k_prolong_cell<DIM, PER, R><<<grid, tpb, prolong_cell_smem<DIM, PER, R>(cx), st>>>(cx, fx, x, out, N, acc);
-  count_launch();
+  prolong_cell_go<DIM, PER, R>(cx, fx, N, x, out, acc, st);
 }
 template <int DIM, bool PER, class R>
 void launch_restrict_face(const Geo& gf, int N, Face3<R> in, FaceW<R> out, cudaStream_t st) {
@@ -861,10 +880,15 @@ void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int ac
   for (int k = 0; k < DIM; ++k) {
     const int rows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
     const dim3 grid(1, (rows + kProlongWarps - 1) / kProlongWarps, N);
-    const size_t shm = (size_t)kProlongWarps * (DIM == 3 ? 4 : 2) * cx.fe(k, DIM - 1) * sizeof(R);
-    if (shm > 48 * 1024)
-      cudaFuncSetAttribute(k_prolong_face<DIM, PER, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-    k_prolong_face<DIM, PER, R><<<grid, 32 * kProlongWarps, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
+    const size_t shm = (size_t)kProlongWarps * cx.fe(k, DIM - 1) * sizeof(R);
+    if (shm > 48 * 1024) {
+      cudaFuncSetAttribute(k_prolong_face<DIM, PER, R, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+      cudaFuncSetAttribute(k_prolong_face<DIM, PER, R, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    }
+    if (fx.fe(k, DIM - 1) <= 192)
+      k_prolong_face<DIM, PER, R, 3><<<grid, 32 * kProlongWarps, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
+    else
+      k_prolong_face<DIM, PER, R, 5><<<grid, 32 * kProlongWarps, shm, st>>>(cx, fx, k, in.c[k], out.c[k], N, acc);
     count_launch();
   }
 }
@@ -1069,10 +1093,7 @@ struct PoissonMG {
     k_resid_restrict<DIM, PER, R><<<grid_for(cx.cells(), 256), 256, 0, st>>>(ix, cx, h, p[li], rhs[li], rhs[li + 1]); count_launch();
     vcycle(li + 1, true, st);
     {
-      int tpb;
-      const dim3 pg = prolong_cell_grid(ix, 1, tpb);
-      k_prolong_cell<DIM, PER, R><<<pg, tpb, prolong_cell_smem<DIM, PER, R>(cx), st>>>(cx, ix, p[li + 1], p[li], 1, 1);
-      count_launch();
+      prolong_cell_go<DIM, PER, R>(cx, ix, 1, p[li + 1], p[li], 1, st);
     }
     k_jacobi<DIM, PER, R><<<gb, 256, 0, st>>>(ix, h, om, p[li], rhs[li], tmp[li], 0); count_launch();
     k_jacobi<DIM, PER, R><<<gb, 256, 0, st>>>(ix, h, om, tmp[li], rhs[li], p[li], 0); count_launch();
