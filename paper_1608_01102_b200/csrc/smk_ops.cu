@@ -282,6 +282,7 @@ __device__ __forceinline__ void pro_idx(int I, int n, int& i0, int& i1) {
 // instructions per fine element (the per-element leading-axis work made the
 // first version issue-bound at 1.6 TB/s).
 constexpr int kProlongWarps = 4;
+constexpr int kProlongRows = 2;   // fine rows per warp, loads of both issued up front
 // fine pairs per lane with prefetched old values: MAXP = 3 (nl <= 192) or 5
 // (nl <= 320, longer rows finish in a tail loop), chosen per launch
 
@@ -354,47 +355,60 @@ __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_cell(Ix<DIM, PER
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nl = DIM == 3 ? fx.n2 : fx.n1, cnl = DIM == 3 ? cx.n2 : cx.n1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  R* crow = reinterpret_cast<R*>(smem_raw) + warp * cnl;   // this warp's combined coarse row
+  constexpr int RPW = kProlongRows;
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * RPW * cnl;   // this warp's combined coarse rows
   const int64_t ncc = cx.cells(), ncf = fx.cells();
   const int fr = blockIdx.z;
   const int nrows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
-  const int row = blockIdx.y * kProlongWarps + warp;
-  if (row >= nrows) return;
+  const int rowb = (blockIdx.y * kProlongWarps + warp) * RPW;
+  if (rowb >= nrows) return;
   const R* p = x + (int64_t)fr * ncc;
-  const int F0 = DIM == 3 ? row / fx.n1 : row;
-  const int F1 = DIM == 3 ? row - F0 * fx.n1 : 0;
-  // in-frame offsets in 32 bits (a frame has < 2^31 elements)
-  R* orow = out + (int64_t)fr * ncf + (DIM == 3 ? (F0 * fx.n1 + F1) * fx.n2 : F0 * fx.n1);
-  R old[MAXP][2];
-  pro_old<R, MAXP>(orow, nl, lane, accumulate, old);
-  int a0, a1, b0 = 0, b1 = 0;
-  pro_idx<PER>(F0, cx.n0, a0, a1);
-  if (DIM == 3) pro_idx<PER>(F1, cx.n1, b0, b1);
-  if (DIM == 3) {
-    // axis 0 (a), then axis 1 (b): y_b = 3/4 (a0, b) + 1/4 (a1, b); c = 3/4 y_b0 + 1/4 y_b1
-    const R *r00 = p + (a0 * cx.n1 + b0) * cx.n2, *r01 = p + (a0 * cx.n1 + b1) * cx.n2;
-    const R *r10 = p + (a1 * cx.n1 + b0) * cx.n2, *r11 = p + (a1 * cx.n1 + b1) * cx.n2;
-    for (int l = lane; l < cnl; l += 32) {
-      const R y0 = R(0.75) * r00[l] + R(0.25) * r10[l];
-      const R y1 = R(0.75) * r01[l] + R(0.25) * r11[l];
-      crow[l] = R(0.75) * y0 + R(0.25) * y1;
-    }
-  } else {
-    const R *r0 = p + a0 * cx.n1, *r1 = p + a1 * cx.n1;
-    for (int l = lane; l < cnl; l += 32) crow[l] = R(0.75) * r0[l] + R(0.25) * r1[l];
+  int F0[RPW], F1[RPW];
+  R* orow[RPW];
+  R old[RPW][MAXP][2];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int row = rowb + r < nrows ? rowb + r : rowb;   // past the end: a duplicate, never stored
+    F0[r] = DIM == 3 ? row / fx.n1 : row;
+    F1[r] = DIM == 3 ? row - F0[r] * fx.n1 : 0;
+    // in-frame offsets in 32 bits (a frame has < 2^31 elements)
+    orow[r] = out + (int64_t)fr * ncf + (DIM == 3 ? (F0[r] * fx.n1 + F1[r]) * fx.n2 : F0[r] * fx.n1);
+    pro_old<R, MAXP>(orow[r], nl, lane, accumulate, old[r]);
   }
-  pro_row<PER, R, MAXP>(crow, cnl, false, orow, nl, lane, accumulate, old);
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    R* cr = crow + r * cnl;
+    int a0, a1, b0 = 0, b1 = 0;
+    pro_idx<PER>(F0[r], cx.n0, a0, a1);
+    if (DIM == 3) pro_idx<PER>(F1[r], cx.n1, b0, b1);
+    if (DIM == 3) {
+      // axis 0 (a), then axis 1 (b): y_b = 3/4 (a0, b) + 1/4 (a1, b); c = 3/4 y_b0 + 1/4 y_b1
+      const R *r00 = p + (a0 * cx.n1 + b0) * cx.n2, *r01 = p + (a0 * cx.n1 + b1) * cx.n2;
+      const R *r10 = p + (a1 * cx.n1 + b0) * cx.n2, *r11 = p + (a1 * cx.n1 + b1) * cx.n2;
+      for (int l = lane; l < cnl; l += 32) {
+        const R y0 = R(0.75) * r00[l] + R(0.25) * r10[l];
+        const R y1 = R(0.75) * r01[l] + R(0.25) * r11[l];
+        cr[l] = R(0.75) * y0 + R(0.25) * y1;
+      }
+    } else {
+      const R *r0 = p + a0 * cx.n1, *r1 = p + a1 * cx.n1;
+      for (int l = lane; l < cnl; l += 32) cr[l] = R(0.75) * r0[l] + R(0.25) * r1[l];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r)
+    if (rowb + r < nrows) pro_row<PER, R, MAXP>(crow + r * cnl, cnl, false, orow[r], nl, lane, accumulate, old[r]);
 }
 
 template <int DIM, bool PER>
 inline dim3 prolong_cell_grid(const Ix<DIM, PER>& fx, int N, int& tpb) {
   tpb = 32 * kProlongWarps;
   const int rows = DIM == 3 ? fx.n0 * fx.n1 : fx.n0;
-  return dim3(1, (rows + kProlongWarps - 1) / kProlongWarps, N);
+  return dim3(1, (rows + kProlongWarps * kProlongRows - 1) / (kProlongWarps * kProlongRows), N);
 }
 template <int DIM, bool PER, class R>
 inline size_t prolong_cell_smem(const Ix<DIM, PER>& cx) {
-  return (size_t)kProlongWarps * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
+  return (size_t)kProlongWarps * kProlongRows * (DIM == 3 ? cx.n2 : cx.n1) * sizeof(R);
 }
 
 // face restriction: along the normal take the coincident (even) face, across
@@ -469,49 +483,58 @@ __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_face(Ix<DIM, PER
   const int L = DIM - 1;                             // last (contiguous) axis
   const int nl = fx.fe(k, L), cnl = cx.fe(k, L);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  R* crow = reinterpret_cast<R*>(smem_raw) + warp * cnl;   // this warp's combined coarse row
+  constexpr int RPW = kProlongRows;
+  R* crow = reinterpret_cast<R*>(smem_raw) + warp * RPW * cnl;   // this warp's combined coarse rows
   const int64_t nfc = cx.faces(k), nff = fx.faces(k);
   const int fr = blockIdx.z;
-  const int nrows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
-  const int row = blockIdx.y * kProlongWarps + warp;
-  if (row >= nrows) return;
-  const R* p = in + (int64_t)fr * nfc;
-  int F[3] = {0, 0, 0};
-  if (DIM == 3) {
-    F[0] = row / fx.fe(k, 1);
-    F[1] = row - F[0] * fx.fe(k, 1);
-  } else {
-    F[0] = row;
-  }
   const int fe1 = fx.fe(k, 1), fe2 = DIM == 3 ? fx.fe(k, 2) : 1;
   const int ce1 = cx.fe(k, 1), ce2 = DIM == 3 ? cx.fe(k, 2) : 1;
-  // in-frame offsets in 32 bits (a frame has < 2^31 elements)
-  R* orow = out + (int64_t)fr * nff + (F[0] * fe1 + F[1]) * fe2;
-  R old[MAXP][2];
-  pro_old<R, MAXP>(orow, nl, lane, accumulate, old);
-  int i0[2] = {0, 0}, i1[2] = {0, 0};
-  R w0[2] = {R(1), R(1)}, w1[2] = {R(0), R(0)};
+  const int nrows = DIM == 3 ? fx.fe(k, 0) * fe1 : fx.fe(k, 0);
+  const int rowb = (blockIdx.y * kProlongWarps + warp) * RPW;
+  if (rowb >= nrows) return;
+  const R* p = in + (int64_t)fr * nfc;
+  int F[RPW][2];
+  R* orow[RPW];
+  R old[RPW][MAXP][2];
 #pragma unroll
-  for (int a = 0; a < DIM - 1; ++a) pro_face_axis<DIM, PER, R>(F[a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
-  // sequential axis application over the leading axes (axis 0, then 1); a
-  // weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit
-  const R* rr[2][2];
-#pragma unroll
-  for (int x = 0; x < 2; ++x)
-#pragma unroll
-    for (int y = 0; y < 2; ++y)
-      rr[x][y] = p + ((x ? i1[0] : i0[0]) * ce1 + (DIM == 3 ? (y ? i1[1] : i0[1]) : 0)) * ce2;
-  for (int l = lane; l < cnl; l += 32) {
-    auto ax0 = [&](int y) -> R {
-      const R a = rr[0][y][l];
-      if (w1[0] == R(0)) return a;
-      return w0[0] * a + w1[0] * rr[1][y][l];
-    };
-    R c = ax0(0);
-    if (DIM == 3 && w1[1] != R(0)) c = w0[1] * c + w1[1] * ax0(1);
-    crow[l] = c;
+  for (int r = 0; r < RPW; ++r) {
+    const int row = rowb + r < nrows ? rowb + r : rowb;   // past the end: a duplicate, never stored
+    F[r][0] = DIM == 3 ? row / fe1 : row;
+    F[r][1] = DIM == 3 ? row - F[r][0] * fe1 : 0;
+    // in-frame offsets in 32 bits (a frame has < 2^31 elements)
+    orow[r] = out + (int64_t)fr * nff + (F[r][0] * fe1 + F[r][1]) * fe2;
+    pro_old<R, MAXP>(orow[r], nl, lane, accumulate, old[r]);
   }
-  pro_row<PER, R, MAXP>(crow, cnl, L == k, orow, nl, lane, accumulate, old);
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    int i0[2] = {0, 0}, i1[2] = {0, 0};
+    R w0[2] = {R(1), R(1)}, w1[2] = {R(0), R(0)};
+#pragma unroll
+    for (int a = 0; a < DIM - 1; ++a)
+      pro_face_axis<DIM, PER, R>(F[r][a], cx.n(a), a == k, i0[a], i1[a], w0[a], w1[a]);
+    // sequential axis application over the leading axes (axis 0, then 1); a
+    // weight of exactly (1, 0) reproduces numpy's plain copy bit-for-bit
+    const R* rr[2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+        rr[x][y] = p + ((x ? i1[0] : i0[0]) * ce1 + (DIM == 3 ? (y ? i1[1] : i0[1]) : 0)) * ce2;
+    R* cr = crow + r * cnl;
+    for (int l = lane; l < cnl; l += 32) {
+      auto ax0 = [&](int y) -> R {
+        const R a = rr[0][y][l];
+        if (w1[0] == R(0)) return a;
+        return w0[0] * a + w1[0] * rr[1][y][l];
+      };
+      R c = ax0(0);
+      if (DIM == 3 && w1[1] != R(0)) c = w0[1] * c + w1[1] * ax0(1);
+      cr[l] = c;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r)
+    if (rowb + r < nrows) pro_row<PER, R, MAXP>(crow + r * cnl, cnl, L == k, orow[r], nl, lane, accumulate, old[r]);
 }
 
 // ===========================================================================
@@ -879,8 +902,8 @@ void launch_prolong_face(const Geo& gc, int N, Face3<R> in, FaceW<R> out, int ac
   Ix<DIM, PER> fx(gf), cx(gc);
   for (int k = 0; k < DIM; ++k) {
     const int rows = DIM == 3 ? fx.fe(k, 0) * fx.fe(k, 1) : fx.fe(k, 0);
-    const dim3 grid(1, (rows + kProlongWarps - 1) / kProlongWarps, N);
-    const size_t shm = (size_t)kProlongWarps * cx.fe(k, DIM - 1) * sizeof(R);
+    const dim3 grid(1, (rows + kProlongWarps * kProlongRows - 1) / (kProlongWarps * kProlongRows), N);
+    const size_t shm = (size_t)kProlongWarps * kProlongRows * cx.fe(k, DIM - 1) * sizeof(R);
     if (shm > 48 * 1024) {
       cudaFuncSetAttribute(k_prolong_face<DIM, PER, R, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
       cudaFuncSetAttribute(k_prolong_face<DIM, PER, R, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
