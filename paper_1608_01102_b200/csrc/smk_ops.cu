@@ -5,6 +5,7 @@
 // results agree with the oracle to a few ulps.  All kernels are HBM-bound
 // stencils: one thread per output point, grid-stride, coalesced along the
 // contiguous axis, neighbours served by L1/L2.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstring>
@@ -412,43 +413,72 @@ inline size_t prolong_cell_smem(const Ix<DIM, PER>& cx) {
 }
 
 // face restriction: along the normal take the coincident (even) face, across
-// it average pairs; axes processed in order
+// it average pairs; axes processed in order.  One warp per
+// coarse row of the leading axes (component blockIdx.x, frame blockIdx.z):
+// the row's 1-4 fine source rows are fixed, so each lane only walks the
+// contiguous axis -- a float2 load per fine row when that axis is an across
+// axis (even fine row length), a scalar load of the coincident face when it
+// is the normal.  Same expressions, same axis order as per-element code.
+constexpr int kRestrictWarps = 4;
 template <int DIM, bool PER, class R>
-__global__ void k_restrict_face(Ix<DIM, PER> fx, Ix<DIM, PER> cx, Face3<R> in, FaceW<R> out, int N) {
-  const int k = blockIdx.y;
-  const int64_t nfc = cx.faces(k), nff = fx.faces(k);
+__global__ void __launch_bounds__(32 * kRestrictWarps) k_restrict_face(Ix<DIM, PER> fx, Ix<DIM, PER> cx, Face3<R> in,
+                                                                      FaceW<R> out, int N) {
+  constexpr int L = DIM - 1;   // contiguous axis
+  const int k = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ce1 = cx.fe(k, 1), ce2 = DIM == 3 ? cx.fe(k, 2) : 1;
+  const int fe1 = fx.fe(k, 1), fe2 = DIM == 3 ? fx.fe(k, 2) : 1;
+  const int crows = DIM == 3 ? cx.fe(k, 0) * ce1 : cx.fe(k, 0);
+  const int row = blockIdx.y * kRestrictWarps + warp;
+  if (row >= crows) return;
   const int fr = blockIdx.z;
-  SMK_FRAME_LOOP(e, nfc) {
-    const int64_t t = (int64_t)fr * nfc + e;
-    int c[3];
-    cx.face_idx32(k, e, c);
-    const R* p = in.c[k] + (int64_t)fr * nff;
-    // candidate fine indices per axis
-    int lo[3], cnt[3];
+  const int C0 = DIM == 3 ? row / ce1 : row;
+  const int C1 = DIM == 3 ? row - C0 * ce1 : 0;
+  const int cnl = cx.fe(k, L);
+  // fine rows: axis 0 picks 2 C0 (+1 across), axis 1 (3D) 2 C1 (+1 across)
+  const int n0 = k == 0 ? 1 : 2, n1 = DIM == 3 ? (k == 1 ? 1 : 2) : 1;
+  const R* p = in.c[k] + (int64_t)fr * fx.faces(k);
+  const R* fr_[2][2];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      if (a >= DIM) { lo[a] = 0; cnt[a] = 1; continue; }
-      lo[a] = 2 * c[a];
-      cnt[a] = (a == k) ? 1 : 2;
-    }
-    // apply axis 0 first, then 1, then 2 (matching numpy's sequential passes)
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 2; ++y)
+      fr_[x][y] = p + (DIM == 3 ? ((2 * C0 + (x < n0 ? x : 0)) * fe1 + 2 * C1 + (y < n1 ? y : 0)) * fe2
+                                 : (2 * C0 + (x < n0 ? x : 0)) * fe1);
+  R* o = out.c[k] + (int64_t)fr * cx.faces(k) + (DIM == 3 ? (C0 * ce1 + C1) * ce2 : C0 * ce1);
+  const bool across = k != L;   // contiguous axis averages pairs
+  for (int l = lane; l < cnl; l += 32) {
+    // v[y][e]: axis 0 applied (fine row pair x), fine element 2l + e
     R v[2][2];
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (b >= cnt[1] || e >= cnt[2]) { v[b][e] = R(0); continue; }
-        int j = lo[1] + b, l = lo[2] + e;
-        v[b][e] = (cnt[0] == 1) ? p[fx.face_off(k, lo[0], j, l)]
-                                : R(0.5) * (p[fx.face_off(k, lo[0], j, l)] + p[fx.face_off(k, lo[0] + 1, j, l)]);
+    for (int y = 0; y < 2; ++y) {
+      if (y >= n1) { v[y][0] = v[y][1] = R(0); continue; }
+      R a0, a1, b0 = R(0), b1 = R(0);
+      if (across) {
+        if constexpr (sizeof(R) == 4) {
+          const float2 t = reinterpret_cast<const float2*>(fr_[0][y])[l];
+          a0 = t.x; a1 = t.y;
+          if (n0 == 2) { const float2 u = reinterpret_cast<const float2*>(fr_[1][y])[l]; b0 = u.x; b1 = u.y; }
+        } else {
+          const double2 t = reinterpret_cast<const double2*>(fr_[0][y])[l];
+          a0 = t.x; a1 = t.y;
+          if (n0 == 2) { const double2 u = reinterpret_cast<const double2*>(fr_[1][y])[l]; b0 = u.x; b1 = u.y; }
+        }
+      } else {
+        a0 = fr_[0][y][2 * l];
+        a1 = R(0);
+        if (n0 == 2) b0 = fr_[1][y][2 * l];
       }
-    R w0 = (cnt[1] == 1) ? v[0][0] : R(0.5) * (v[0][0] + v[1][0]);
+      v[y][0] = n0 == 1 ? a0 : R(0.5) * (a0 + b0);
+      v[y][1] = n0 == 1 ? a1 : R(0.5) * (a1 + b1);
+    }
+    const R w0 = n1 == 1 ? v[0][0] : R(0.5) * (v[0][0] + v[1][0]);
     R res = w0;
-    if (cnt[2] == 2) {
-      R w1 = (cnt[1] == 1) ? v[0][1] : R(0.5) * (v[0][1] + v[1][1]);
+    if (across) {
+      const R w1 = n1 == 1 ? v[0][1] : R(0.5) * (v[0][1] + v[1][1]);
       res = R(0.5) * (w0 + w1);
     }
-    out.c[k][t] = res;
+    o[l] = res;
   }
 }
 
@@ -893,7 +923,10 @@ template <int DIM, bool PER, class R>
 void launch_restrict_face(const Geo& gf, int N, Face3<R> in, FaceW<R> out, cudaStream_t st) {
   Geo gc = coarsen(gf);
   Ix<DIM, PER> fx(gf), cx(gc);
-  k_restrict_face<DIM, PER, R><<<frame_grid(cx.faces(0), N, 256, DIM), 256, 0, st>>>(fx, cx, in, out, N);
+  int rows = 0;
+  for (int k = 0; k < DIM; ++k) rows = std::max(rows, DIM == 3 ? cx.fe(k, 0) * cx.fe(k, 1) : cx.fe(k, 0));
+  const dim3 grid(DIM, (rows + kRestrictWarps - 1) / kRestrictWarps, N);
+  k_restrict_face<DIM, PER, R><<<grid, 32 * kRestrictWarps, 0, st>>>(fx, cx, in, out, N);
   count_launch();
 }
 template <int DIM, bool PER, class R>
