@@ -1307,6 +1307,15 @@ __global__ void __launch_bounds__(256) k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, i
       if (i >= N) break;
       const R* xu = xout + (int64_t)(2 * i) * B * M + m;
       const R* xv = xout + (int64_t)(2 * i + 1) * B * M + m;
+      // every load first, then the stores: the state pointers may alias as
+      // far as the compiler knows, so interleaved += would serialise 14
+      // memory round trips per thread
+      R du[B], dv[B], ou[NF], ov[NF];
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        du[q] = xu[(int64_t)q * M];
+        dv[q] = xv[(int64_t)q * M];
+      }
 #pragma unroll
       for (int k = 0; k < DIM; ++k)
 #pragma unroll
@@ -1314,12 +1323,23 @@ __global__ void __launch_bounds__(256) k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, i
           const int qq = 2 * k + sd;
           if (w[qq]) continue;
           const int64_t o = (int64_t)i * nf[k] + fo[qq];
-          s.U[k][o] += xu[(int64_t)qq * M];
-          s.V[k][o] += xv[(int64_t)qq * M];
+          ou[qq] = s.U[k][o];
+          ov[qq] = s.V[k][o];
         }
       const int64_t oc = (int64_t)i * ncl + co;
-      s.P[oc] += xu[(int64_t)NF * M];
-      s.PB[oc] += xv[(int64_t)NF * M];
+      const R op = s.P[oc], opb = s.PB[oc];
+#pragma unroll
+      for (int k = 0; k < DIM; ++k)
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd) {
+          const int qq = 2 * k + sd;
+          if (w[qq]) continue;
+          const int64_t o = (int64_t)i * nf[k] + fo[qq];
+          s.U[k][o] = ou[qq] + du[qq];
+          s.V[k][o] = ov[qq] + dv[qq];
+        }
+      s.P[oc] = op + du[NF];
+      s.PB[oc] = opb + dv[NF];
     }
   }
 }
