@@ -219,6 +219,15 @@ int smk_nso_level_residual(smk_nso* h, int level, const smk_state* s, const void
 int smk_nso_level_color_pass(smk_nso* h, int level, int colour, const smk_state* s, const void* const vprev[],
                              const void* const unext[], const void* const vs[], const smk_residual* rhs,
                              void* stream);
+/* ---------------- advection optimisation (ao.py) ---------------- */
+
+/* One separable pass of the keyframe metric (GaussianMetric._filter,
+ * ao.py:100-104): x viewed as (outer, n, inner), y = alpha * op(M) x along
+ * the middle axis + beta * y (y not read when beta == 0), op(M) = M (n x n,
+ * C order) or M^T when transpose != 0.  GaussianMetric.apply / quad
+ * (ao.py:106-120) are 2*dim such passes per pyramid level.  x != y. */
+int smk_axis_filter(int dtype, int64_t outer, int n, int64_t inner, const void* M, int transpose, double alpha,
+                    double beta, const void* x, void* y, void* stream);
 /* y = a * x + b * y over n elements (state algebra of the slab V-cycle) */
 int smk_axpby(int dtype, void* y, const void* x, double a, double b, int64_t n, void* stream);
 

@@ -160,3 +160,44 @@ def ao_sweep(g, vstar, v_guiding, rho0, targets, metric, K, dt,
         for k in range(g.dim):
             vs[k][i - 1] = proj[k]
     return vs, mu, rho, ks
+
+
+def ao_objective(g, vstar, v_guiding, rho0, targets, metric, K, dt, tol=1e-5, cap=128):
+    """``ao.py:173-183``: 0.5 sum |rho_i - rho*_i|_C^2 + (K/2) |v - v*|^2."""
+    rho, _ = rollout(g, vstar, rho0, dt, tol, cap)
+    mismatch = sum(metric.quad(rho[i] - t) for i, t in targets.items())
+    vterm = sum(float(np.vdot(a - b, a - b)) for a, b in zip(v_guiding, vstar))
+    return 0.5 * mismatch + 0.5 * K * vterm
+
+
+def solve_ao(g, v_guiding, rho0, targets, metric, K, dt, iters=2, safeguard=False,
+             projection_tol=1e-9, tol=1e-5, cap=128):
+    """``ao.py:216-254``: fixed sweeps; with the safeguard each sweep's v* is
+    blended with the previous one, halving alpha (> 1/64) until the objective
+    does not increase.  Returns (vstar, mu, rho, ks)."""
+    n = v_guiding[0].shape[0]
+    vs = tuple(c.copy() for c in v_guiding)
+    mu = np.zeros((n,) + g.res)
+    rho = np.broadcast_to(rho0, (n + 1,) + g.res).copy()
+    ks = []
+    obj = ao_objective(g, vs, v_guiding, rho0, targets, metric, K, dt, tol, cap) if safeguard else None
+    for _ in range(iters):
+        nv, nmu, nrho, nks = ao_sweep(g, vs, v_guiding, rho0, targets, metric, K, dt,
+                                      projection_tol, tol, cap)
+        if not safeguard:
+            vs, mu, rho, ks = nv, nmu, nrho, nks
+            continue
+        alpha, accepted = 1.0, None
+        while alpha > 1.0 / 64.0:
+            blend = tuple((1 - alpha) * a + alpha * b for a, b in zip(vs, nv))
+            o = ao_objective(g, blend, v_guiding, rho0, targets, metric, K, dt, tol, cap)
+            if o <= obj * (1 + 1e-12) + 1e-300:
+                accepted = (blend, o)
+                break
+            alpha *= 0.5
+        if accepted is None:
+            break
+        vs, obj = accepted
+        mu = nmu
+        rho, ks = rollout(g, vs, rho0, dt, tol, cap)
+    return vs, mu, rho, ks

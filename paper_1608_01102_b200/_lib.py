@@ -105,6 +105,7 @@ SIGNATURES = {
     "smk_nso_level_residual": (I, [P, I, PS, P, P, P, PR, PR, P]),
     "smk_nso_level_color_pass": (I, [P, I, I, PS, P, P, P, PR, P]),
     "smk_axpby": (I, [I, P, P, D, D, I64, P]),
+    "smk_axis_filter": (I, [I, I64, I, I64, P, I, D, D, P, P, P]),
 }
 
 _lib = None

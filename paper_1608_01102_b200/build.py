@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libsmk.so")
-SOURCES = ["smk_ops.cu", "smk_stfas.cu"]
+SOURCES = ["smk_ops.cu", "smk_stfas.cu", "smk_ao.cu"]
 HEADERS = ["smk_common.cuh", "smk_dispatch.cuh", "smk_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",

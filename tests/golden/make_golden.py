@@ -146,6 +146,42 @@ def main():
         put(tag, "ks", np.array(res.ks))
         put(tag, "metric_apply", metric.apply(rho0 - target))
 
+    # solve_ao (2D Neumann, plain and safeguarded) + objective, and a 3D
+    # periodic metric apply / quad
+    for tag, safeguard, iters in [("aos0", False, 2), ("aos1", True, 3)]:
+        spec = F.GridSpec(2, (8, 8), 0.125, "neumann")
+        rng = np.random.default_rng(3100 + iters)
+        n = 4
+        guiding = [F.project_arrays(spec, smooth(spec, rng, 0.3), 1e-11)
+                   for _ in range(n)]
+        guiding = tuple(np.stack([gd[k] for gd in guiding]) for k in range(2))
+        g2 = np.meshgrid(*[(np.arange(m) + 0.5) * spec.h for m in spec.res],
+                         indexing="ij")
+        rho0 = np.exp(-((g2[0] - 0.35) ** 2 + (g2[1] - 0.5) ** 2) / 0.02)
+        t2 = np.exp(-((g2[0] - 0.5) ** 2 + (g2[1] - 0.55) ** 2) / 0.02)
+        t4 = np.exp(-((g2[0] - 0.65) ** 2 + (g2[1] - 0.5) ** 2) / 0.02)
+        kf = AO.KeyframeSet(n, {2: t2, 4: t4})
+        metric = AO.GaussianMetric(spec)
+        cfg = AO.AoConfig(K=5.0, dt=0.5, iters=iters, safeguard=safeguard)
+        res = AO.solve_ao(spec, guiding, rho0, kf, metric, cfg)
+        put(tag, "guiding", guiding)
+        put(tag, "rho0", rho0)
+        put(tag, "t2", t2)
+        put(tag, "t4", t4)
+        put(tag, "vstar", res.vstar)
+        put(tag, "mu", res.mu)
+        put(tag, "rho", res.rho)
+        put(tag, "ks", np.array(res.ks))
+        put(tag, "obj0", np.array(AO.ao_objective(spec, guiding, guiding, kf, metric, cfg, rho0)))
+        put(tag, "obj", np.array(AO.ao_objective(spec, res.vstar, guiding, kf, metric, cfg, rho0)))
+    spec = F.GridSpec(3, (8, 8, 16), 0.125, "periodic")
+    rng = np.random.default_rng(3200)
+    x = rng.standard_normal(spec.res)
+    metric = AO.GaussianMetric(spec, levels=2, weights=(1.0, 0.5))
+    put("met3", "x", x)
+    put("met3", "apply", metric.apply(x))
+    put("met3", "quad", np.array(metric.quad(x)))
+
     np.savez_compressed(OUT, **out)
     print("wrote", OUT, len(out), "arrays")
 

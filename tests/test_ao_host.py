@@ -1,0 +1,36 @@
+"""Host-side logic of the AO drop-in (no GPU): the per-axis filter matrices
+and the keyframe / metric argument validation, against the oracle and the
+reference's error behaviour (ao.py:27-45, :48-95)."""
+
+import numpy as np
+import pytest
+
+from oracle import sim
+
+
+@pytest.mark.parametrize("n,sigma,periodic", [(8, 1.0, True), (8, 1.0, False), (16, 4.0, False),
+                                             (32, 8.0, True), (128, 32.0, False)])
+def test_filter_matrix_matches_oracle(n, sigma, periodic):
+    from paper_1608_01102_b200.ao import _filter_matrix
+    m = _filter_matrix(n, sigma, periodic)
+    assert np.array_equal(m, sim.axis_matrix(n, sigma, periodic))
+    assert np.allclose(m.sum(axis=1), 1.0, rtol=0, atol=1e-14)
+
+
+def test_keyframe_and_metric_validation():
+    from paper_1608_01102_b200.ao import GaussianMetric, KeyframeSet
+    from paper_1608_01102_b200.fields import GridSpec
+    with pytest.raises(ValueError):
+        KeyframeSet(3, {})
+    with pytest.raises(ValueError):
+        KeyframeSet(3, {0: np.zeros((8, 8))})
+    with pytest.raises(ValueError):
+        KeyframeSet(3, {1: -np.ones((8, 8))})
+    kf = KeyframeSet(3, {1: np.zeros((8, 8)), 3: np.ones((8, 8))})
+    assert list(kf.flags) == [False, True, False, True]
+    spec = GridSpec(2, (16, 16), 1 / 16, "neumann")
+    assert GaussianMetric(spec).levels == 3
+    with pytest.raises(ValueError):
+        GaussianMetric(spec, levels=0)
+    with pytest.raises(ValueError):
+        GaussianMetric(spec, levels=2, weights=(1.0,))

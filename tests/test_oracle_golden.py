@@ -90,3 +90,31 @@ def test_ao_sweep(golden, tag):
     assert rel_err(rho, c["rho"]) < 1e-12
     assert rel_err(mu, c["mu"]) < 1e-12
     assert rel_err(vs, c.comps("vstar")) < 1e-10
+
+
+@pytest.mark.parametrize("tag,safeguard,iters", [("aos0", False, 2), ("aos1", True, 3)])
+def test_solve_ao(golden, tag, safeguard, iters):
+    from oracle.grid import Grid
+    c = GoldenCase(golden, tag)
+    g = Grid(2, (8, 8), 0.125, "neumann")
+    guiding = c.comps("guiding")
+    targets = {2: c["t2"], 4: c["t4"]}
+    metric = sim.GaussianMetric(g)
+    obj0 = sim.ao_objective(g, guiding, guiding, c["rho0"], targets, metric, 5.0, 0.5)
+    assert abs(obj0 - float(c["obj0"])) <= 1e-13 * abs(float(c["obj0"]))
+    vs, mu, rho, ks = sim.solve_ao(g, guiding, c["rho0"], targets, metric, 5.0, 0.5, iters, safeguard)
+    assert list(ks) == [int(k) for k in c["ks"]]
+    assert rel_err(vs, c.comps("vstar")) < 1e-10
+    assert rel_err(mu, c["mu"]) < 1e-10
+    assert rel_err(rho, c["rho"]) < 1e-11
+    obj = sim.ao_objective(g, vs, guiding, c["rho0"], targets, metric, 5.0, 0.5)
+    assert abs(obj - float(c["obj"])) <= 1e-10 * abs(float(c["obj"]))
+
+
+def test_metric_3d_periodic(golden):
+    from oracle.grid import Grid
+    c = GoldenCase(golden, "met3")
+    g = Grid(3, (8, 8, 16), 0.125, "periodic")
+    metric = sim.GaussianMetric(g, levels=2, weights=(1.0, 0.5))
+    assert rel_err(metric.apply(c["x"]), c["apply"]) < 1e-13
+    assert abs(metric.quad(c["x"]) - float(c["quad"])) <= 1e-13 * float(c["quad"])
