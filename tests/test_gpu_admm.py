@@ -1,0 +1,79 @@
+"""GPU ADMM outer loop (admm.run) vs the oracle restatement
+(oracle/admm.py) — B200, fp64.
+
+The inner NSO solves run to ||f||_inf <= 1e-9 on both sides, so the two
+loops see the same iterates up to the solver tolerance: per-iteration
+visual differences and the final fields agree to 1e-6 relative, the outer
+iteration count and the convergence flag exactly.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+N, DT, K, R = 4, 0.25, 10.0, 1.0
+
+
+def _problem():
+    xs = np.meshgrid(*[(np.arange(8) + 0.5) / 8] * 2, indexing="ij")
+    rho0 = np.exp(-((xs[0] - 0.4) ** 2 + (xs[1] - 0.5) ** 2) / 0.02)
+    target = np.exp(-((xs[0] - 0.6) ** 2 + (xs[1] - 0.5) ** 2) / 0.02)
+    return rho0, target
+
+
+def _both(eps_admm, max_outer, tmp_path=None):
+    from oracle import admm as oadmm
+    from oracle.grid import Grid
+    from paper_1608_01102_b200 import admm, ao, fields
+    from paper_1608_01102_b200.errors import MaxIterations
+    rho0, target = _problem()
+    g = Grid(2, (8, 8), 0.125, "neumann")
+    ref = oadmm.run(g, rho0, {N: target}, N, DT, K=K, r=R, eps_stfas=1e-9, eps_admm=eps_admm,
+                    max_outer=max_outer, nso_cycle_budget=100)
+    spec = fields.GridSpec(2, (8, 8), 0.125, "neumann")
+    cfg = admm.AdmmConfig(dt=DT, K=K, r=R, eps_stfas=1e-9, eps_admm=eps_admm, max_outer=max_outer,
+                          nso_cycle_budget=100)
+    try:
+        res = admm.run(spec, rho0, ao.KeyframeSet(N, {N: target}), cfg)
+    except MaxIterations as e:
+        res = e.result
+        assert not ref["converged"]
+    return ref, res
+
+
+def _compare(ref, res):
+    assert res.converged == ref["converged"]
+    assert len(res.logs) == len(ref["logs"])
+    for a, b in zip(res.logs, ref["logs"]):
+        assert a["outer_iter"] == b["outer_iter"]
+        assert abs(a["visual_diff"] - b["visual_diff"]) <= 1e-6 * b["visual_diff"]
+        assert abs(a["ao_obj"] - b["ao_obj"]) <= 1e-8 * abs(b["ao_obj"])
+        assert a["nso_resid"] <= 1e-9
+    t = lambda xs: tuple(x.cpu().numpy() for x in xs)
+    assert rel_err(res.rho.cpu().numpy(), ref["rho"]) < 1e-8
+    assert rel_err(t(res.vstar), ref["vstar"]) < 1e-6
+    assert rel_err(t(res.v), ref["v"]) < 1e-6
+    assert rel_err(t(res.u), ref["state"].U) < 1e-6
+    lam = ref["lam"]
+    if max(float(np.abs(c).max()) for c in lam) > 0:
+        assert rel_err(t(res.lam), lam) < 1e-6
+
+
+def test_admm_converges_like_oracle(tmp_path):
+    ref, res = _both(None, 8)
+    assert ref["converged"]
+    _compare(ref, res)
+    path = tmp_path / "admm.csv"
+    res.write_log_csv(path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "outer_iter,ao_obj,nso_resid,visual_diff,wall_s"
+    assert len(lines) == 1 + len(res.logs)
+
+
+def test_admm_max_iterations_with_multiplier_updates():
+    ref, res = _both(1e-7, 3)
+    assert not ref["converged"] and len(res.logs) == 3
+    _compare(ref, res)
