@@ -8,9 +8,21 @@
 
 namespace smk {
 
-// device allocations released together (operator-level scratch)
+// device allocations released together.  Scratch(st) is operator-level
+// scratch: its buffers come from a process-wide pool and go back to it on
+// release with an event recorded on `st`, so a later call reuses them with no
+// cudaMalloc / cudaFree (cudaFree synchronises the whole device): on the same
+// stream stream order makes reuse safe, on another stream the taker waits on
+// the event.  A default-constructed Scratch (long-lived solver memory) owns
+// plain cudaMalloc allocations.
 struct Scratch {
   std::vector<std::pair<void*, size_t>> bufs;
+  cudaStream_t st = nullptr;
+  bool pooled = false;
+  Scratch() = default;
+  explicit Scratch(cudaStream_t s) : st(s), pooled(true) {}
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
   void* get(size_t bytes);
   void release();
   ~Scratch();

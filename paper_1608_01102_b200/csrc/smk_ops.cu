@@ -810,16 +810,81 @@ using namespace smk;
 
 namespace smk {
 
+namespace {
+struct PoolEntry {
+  void* p;
+  cudaStream_t st;
+  cudaEvent_t ev;
+};
+std::mutex g_pool_mu;
+std::multimap<size_t, PoolEntry> g_pool;   // rounded size -> free buffers
+constexpr size_t kPoolMax = size_t(1) << 30;
+
+size_t pool_round(size_t b) {
+  b = b < 256 ? 256 : b;
+  return (b + 4095) & ~size_t(4095);
+}
+}  // namespace
+
 Scratch::~Scratch() { release(); }
 void Scratch::release() {
-  for (auto& b : bufs)
-    if (b.first) cudaFree(b.first);
+  for (auto& b : bufs) {
+    if (!b.first) continue;
+    if (pooled && b.second <= kPoolMax) {
+      cudaEvent_t ev = nullptr;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(ev, st) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_pool.emplace(b.second, PoolEntry{b.first, st, ev});
+        continue;
+      }
+      cudaGetLastError();
+      if (ev) cudaEventDestroy(ev);
+      cudaStreamSynchronize(st);
+    }
+    cudaFree(b.first);
+  }
   bufs.clear();
 }
 void* Scratch::get(size_t bytes) {
+  const size_t r = pool_round(bytes);
+  if (pooled && r <= kPoolMax) {
+    PoolEntry e{nullptr, nullptr, nullptr};
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      auto it = g_pool.find(r);
+      if (it != g_pool.end()) {
+        e = it->second;
+        g_pool.erase(it);
+      }
+    }
+    if (e.p) {
+      if (e.st != st) cudaStreamWaitEvent(st, e.ev, 0);
+      cudaEventDestroy(e.ev);
+      bufs.push_back({e.p, r});
+      return e.p;
+    }
+  }
   void* p = nullptr;
-  if (cudaMalloc(&p, bytes < 256 ? 256 : bytes) != cudaSuccess) return nullptr;
-  bufs.push_back({p, bytes});
+  if (cudaMalloc(&p, r) != cudaSuccess) {
+    cudaGetLastError();
+    // out of memory: hand the pooled buffers back to the driver and retry
+    std::multimap<size_t, PoolEntry> drop;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      drop.swap(g_pool);
+    }
+    for (auto& kv : drop) {
+      cudaEventSynchronize(kv.second.ev);
+      cudaEventDestroy(kv.second.ev);
+      cudaFree(kv.second.p);
+    }
+    if (cudaMalloc(&p, r) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  bufs.push_back({p, r});
   return p;
 }
 
@@ -1115,7 +1180,7 @@ struct PoissonMG {
   const R* pinv = nullptr;
   bool ok = true;
 
-  explicit PoissonMG(const Geo& g) {
+  PoissonMG(const Geo& g, cudaStream_t st) : scratch(st) {
     lv.push_back(g);
     while (can_coarsen(lv.back())) lv.push_back(coarsen(lv.back()));
     for (size_t i = 0; i < lv.size(); ++i) {
@@ -1160,11 +1225,11 @@ struct PoissonMG {
 template <int DIM, bool PER, class R>
 int poisson_solve(const Geo& g, const R* rhs_in, R* p_out, double tol, int max_cycles, int* cycles,
                   double* residual, cudaStream_t st) {
-  PoissonMG<DIM, PER, R> mg(g);
+  PoissonMG<DIM, PER, R> mg(g, st);
   if (!mg.ok) { set_error("poisson: allocation failed"); return SMK_ERR_CUDA; }
   Ix<DIM, PER> ix(g);
   int64_t n = ix.cells();
-  Scratch sc;
+  Scratch sc(st);
   double* parts = (double*)sc.get(sizeof(double) * 600);
   void* scal = sc.get(16);
   // rhs - mean(rhs)
@@ -1213,7 +1278,7 @@ int project(const Geo& g, Face3<R> in, FaceW<R> out, double tol, int* cycles, do
     dim3 grid(grid_for(ix.faces(0), 256), DIM);
     k_zero_walls<DIM, PER, R><<<grid, 256, 0, st>>>(ix, out, 1); count_launch();
   }
-  Scratch sc;
+  Scratch sc(st);
   int64_t n = ix.cells();
   R* dv = (R*)sc.get(n * sizeof(R));
   R* phi = (R*)sc.get(n * sizeof(R));
@@ -1243,7 +1308,7 @@ int advect(const Geo& g, Face3<R> v, const R* rho, R* out, double dt, double tol
            int transpose, int* k_used, double* last, cudaStream_t st) {
   Ix<DIM, PER> ix(g);
   int64_t n = ix.cells();
-  Scratch sc;
+  Scratch sc(st);
   R* t0 = (R*)sc.get(n * sizeof(R));
   R* t1 = (R*)sc.get(n * sizeof(R));
   R* norms = (R*)sc.get(sizeof(R) * (size_t)(cap + 2));
@@ -1300,7 +1365,7 @@ int advect_v_T(const Geo& g, Face3<R> v, const R* rho, const R* mu, FaceW<R> out
   Ix<DIM, PER> ix(g);
   int64_t n = ix.cells();
   if (K < 1) { set_error("advect_v_T: k must be >= 1"); return SMK_ERR_ARG; }
-  Scratch sc;
+  Scratch sc(st);
   R* xs = (R*)sc.get((size_t)K * n * sizeof(R));
   R* ys = (R*)sc.get((size_t)K * n * sizeof(R));
   if (!xs || !ys) { set_error("advect_v_T: allocation failed"); return SMK_ERR_CUDA; }
@@ -1322,7 +1387,7 @@ int sim_step(const Geo& g, Face3<R> v_in, const R* rho, Face3<R> u_in, double dt
              double trunc_tol, int trunc_cap, FaceW<R> v_out, R* p_out, R* rho_out, int* k_used, double* pres,
              cudaStream_t st) {
   Ix<DIM, PER> ix(g);
-  Scratch sc;
+  Scratch sc(st);
   FaceW<R> v, u, w, wn, adv, tgt;
   auto alloc_face = [&](FaceW<R>& f) {
     for (int k = 0; k < 3; ++k) f.c[k] = k < DIM ? (R*)sc.get(ix.faces(k) * sizeof(R)) : nullptr;
@@ -1456,7 +1521,7 @@ int smk_laplacian(const smk_grid* g, int N, const void* p, void* out, void* stre
 
 int smk_inf_norm(int dtype, const void* x, int64_t n, double* out, void* stream) {
   if (dtype != SMK_F64 && dtype != SMK_F32) { set_error("bad dtype"); return SMK_ERR_ARG; }
-  Scratch sc;
+  Scratch sc(ST(stream));
   void* scal = sc.get(16);
   *out = host_absmax(dtype, x, n, ST(stream), scal);
   return cuda_check("smk_inf_norm");
@@ -1464,7 +1529,7 @@ int smk_inf_norm(int dtype, const void* x, int64_t n, double* out, void* stream)
 
 int smk_dot(int dtype, const void* x, const void* y, int64_t n, double* out, void* stream) {
   if (dtype != SMK_F64 && dtype != SMK_F32) { set_error("bad dtype"); return SMK_ERR_ARG; }
-  Scratch sc;
+  Scratch sc(ST(stream));
   double* parts = (double*)sc.get(sizeof(double) * 600);
   *out = host_sum(dtype, x, y, n, ST(stream), parts);
   return cuda_check("smk_dot");
