@@ -452,3 +452,51 @@ def solve_nso(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None,
         if r.inf() <= tol:
             return NsoResult(st, hist, True)
     return NsoResult(st, hist, False)
+
+
+LM_WINDOW, LM_STALL, LM_MIN_SHIFT = 3, 0.95, 1e-3
+
+
+def solve_nso_lm(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None, stall=LM_STALL):
+    """SPEC.md:347 LM safeguard as frozen in DESIGN §11 (proximal shift):
+    while the per-cycle reduction factor over 3 cycles exceeds 0.95 the K/r
+    blocks get a shift sigma (K, doubled while stalled, halved while
+    progressing, dropped below 1e-3 K); a shifted V-cycle solves the problem
+    with K + sigma and guide (K v* + sigma v^k)/(K + sigma).  The stop test
+    uses the undamped residual."""
+    import dataclasses
+    levels = build_levels(pb, n_levels if n_levels else 99)
+    if st is None:
+        st = zero_state(pb.g, pb.N)
+    N = pb.N
+    r = kkt_residual(pb, st)
+    hist = [(0, r.inf(), r.l2())]
+    if hist[0][1] <= eps:
+        return NsoResult(st, hist, True)
+    sigma = 0.0
+    for c in range(1, cycle_budget + 1):
+        if sigma > 0:
+            K2 = pb.K + sigma
+            guide = []
+            for k in range(pb.g.dim):
+                gk = pb.vstar[k].copy()
+                gk[1:] = (pb.K / K2) * pb.vstar[k][1:] + (sigma / K2) * st.V[k][:N - 1]
+                guide.append(gk)
+            pd = dataclasses.replace(pb, K=K2, vstar=tuple(guide))
+            st = gauge_fix(vcycle(build_levels(pd, n_levels if n_levels else 99), 0, st))
+        else:
+            st = gauge_fix(vcycle(levels, 0, st))
+        r = kkt_residual(pb, st)
+        hist.append((c, r.inf(), r.l2()))
+        if r.inf() <= eps:
+            return NsoResult(st, hist, True)
+        if c >= LM_WINDOW:
+            prev = hist[c - LM_WINDOW][1]
+            factor = (r.inf() / prev) ** (1.0 / LM_WINDOW) if prev > 0 else 0.0
+            if factor > stall:
+                sigma = pb.K if sigma == 0 else 2.0 * sigma
+            elif sigma > 0:
+                sigma *= 0.5
+                if sigma < LM_MIN_SHIFT * pb.K:
+                    sigma = 0.0
+    return NsoResult(st, hist, False)

@@ -25,7 +25,7 @@ from . import _dev
 from .ao import AoConfig, GaussianMetric, KeyframeSet, _axpby, _objective_dev, _rollout_dev, solve_ao
 from .errors import MaxIterations, SmokeCtrlError
 from .fields import dot_fields, inf_norm
-from .nso import SpacetimeState, StfasConfig, StfasHierarchy
+from .nso import SpacetimeState, StfasConfig, StfasHierarchy, _solve_lm
 
 
 @dataclass
@@ -47,6 +47,7 @@ class AdmmConfig:
     relative_stfas: bool = False    # fp32: eps_STFAS relative to ||f_0||_inf
     n_levels: int = 99
     projection_tol: float = 1e-9
+    lm: bool = False                # LM safeguard of the STFAS solves (nso._solve_lm)
 
 
 @dataclass
@@ -114,7 +115,8 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
     eps_admm = cfg.eps_admm if cfg.eps_admm is not None else inf_norm(r0) / 100.0
     aocfg = AoConfig(K=cfg.K, dt=cfg.dt, iters=cfg.ao_iters, safeguard=cfg.ao_safeguard,
                      projection_tol=cfg.projection_tol)
-    hier = StfasHierarchy(spec, StfasConfig(dt=cfg.dt, K=cfg.K, r=cfg.r, n_levels=cfg.n_levels), n, dtype)
+    ncfg = StfasConfig(dt=cfg.dt, K=cfg.K, r=cfg.r, n_levels=cfg.n_levels)
+    hier = StfasHierarchy(spec, ncfg, n, dtype)
     logs = []
     result = None
     prev_aug = None
@@ -128,8 +130,12 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
                 ao_obj = _objective_dev(spec, vstar, guiding, keyframes, metric, aocfg, r0)
                 guide = tuple(_axpby(vc.clone(), lc, -1.0 / cfg.K, 1.0) for vc, lc in zip(vstar, lam))
                 hier.set_guide(v0, guide)
-                hist = hier.solve(s, eps=cfg.eps_stfas, relative=cfg.relative_stfas,
-                                  cycle_budget=cfg.nso_cycle_budget)
+                if cfg.lm:
+                    hist = _solve_lm(spec, ncfg, hier, v0, guide, s, cfg.eps_stfas, cfg.relative_stfas,
+                                     cfg.nso_cycle_budget)
+                else:
+                    hist = hier.solve(s, eps=cfg.eps_stfas, relative=cfg.relative_stfas,
+                                      cycle_budget=cfg.nso_cycle_budget)
             except SmokeCtrlError as e:
                 e.args = (f"outer iteration {it}: {e.args[0] if e.args else ''}",) + e.args[1:]
                 e.outer_iter = it

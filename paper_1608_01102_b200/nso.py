@@ -314,10 +314,11 @@ class NsoResult:
 
 
 def solve_nso(spec, cfg, v0, vstar, s=None, eps=1e-5, cycle_budget=50, relative=False, dtype=None,
-              hierarchy=None):
+              hierarchy=None, lm=False, lm_stall=None):
     """Repeat V-cycles until ||f||_inf <= eps.
 
-    Raises NonConvergence when the cycle budget is exhausted."""
+    Raises NonConvergence when the cycle budget is exhausted.  With ``lm``
+    the Levenberg-Marquardt safeguard of SPEC.md:347 runs (``_solve_lm``)."""
     _dev.require_device()
     N = int(vstar[0].shape[0])
     dt = dtype or (s.dtype if s is not None else (_dev.infer_dtype(vstar) or torch.float64))
@@ -325,5 +326,83 @@ def solve_nso(spec, cfg, v0, vstar, s=None, eps=1e-5, cycle_budget=50, relative=
         s = SpacetimeState.zeros(spec, N, dt)
     hier = hierarchy or StfasHierarchy(spec, cfg, N, dt)
     hier.set_guide(v0, vstar)
-    hist = hier.solve(s, eps=eps, relative=relative, cycle_budget=cycle_budget)
+    if lm:
+        hist = _solve_lm(spec, cfg, hier, v0, vstar, s, eps, relative, cycle_budget,
+                         LM_STALL if lm_stall is None else lm_stall)
+    else:
+        hist = hier.solve(s, eps=eps, relative=relative, cycle_budget=cycle_budget)
     return NsoResult(s, hist, True, hier)
+
+
+LM_WINDOW = 3          # cycles over which the reduction factor is measured
+LM_STALL = 0.95        # per-cycle factor above which the shift is raised
+LM_MIN_SHIFT = 1e-3    # shift (relative to K) below which it is dropped
+
+
+def _solve_lm(spec, cfg, hier, v0, vstar, s, eps, relative, budget, stall=LM_STALL):
+    """SPEC.md:347 LM safeguard, frozen as a proximal shift.
+
+    While the per-cycle reduction factor of ||f||_inf over the last
+    LM_WINDOW cycles exceeds LM_STALL, the K/r blocks get a shift sigma
+    (sigma = K, then doubled while stalled, halved while progressing, dropped
+    below LM_MIN_SHIFT K).  A shifted V-cycle solves the damped problem
+    K' = K + sigma with guide (K v* + sigma v^k) / K' (v^k = the iterate
+    entering the cycle): the K-term becomes K/r (v - v*) + sigma/r (v - v^k),
+    so every fixed point of the damped cycles is the undamped solution.  The
+    stop test always uses the undamped residual.  Raises NonConvergence when
+    the budget is exhausted."""
+    dt = s.dtype
+    v0d, vs = _guide(spec, v0, vstar, dt)
+    ri, r2 = hier.residual_norms(s)
+    hist = [(0, ri, r2)]
+    tol = eps * ri if relative else eps
+    if ri <= tol:
+        return hist
+    sigma = 0.0
+    damped = {}
+    N = s.N
+    try:
+        for c in range(1, budget + 1):
+            if sigma > 0:
+                key = sigma
+                if key not in damped:
+                    dcfg = StfasConfig(**{**cfg.__dict__, "K": cfg.K + sigma})
+                    damped[key] = StfasHierarchy(spec, dcfg, N, dt)
+                hd = damped[key]
+                a, b = cfg.K / (cfg.K + sigma), sigma / (cfg.K + sigma)
+                guide = []
+                for k in range(spec.dim):
+                    g = vs[k].clone()
+                    if N > 1:
+                        _axpby_dev(g[1:], s.V[k][:N - 1], b, a)
+                    guide.append(g)
+                hd.set_guide(v0d, tuple(guide))
+                hd.vcycle(s)
+                hd.gauge_fix(s)
+            else:
+                hier.vcycle(s)
+                hier.gauge_fix(s)
+            ri, r2 = hier.residual_norms(s)
+            hist.append((c, ri, r2))
+            if ri <= tol:
+                return hist
+            if c >= LM_WINDOW:
+                prev = hist[c - LM_WINDOW][1]
+                factor = (ri / prev) ** (1.0 / LM_WINDOW) if prev > 0 else 0.0
+                if factor > stall:
+                    sigma = cfg.K if sigma == 0 else 2.0 * sigma
+                elif sigma > 0:
+                    sigma = 0.5 * sigma
+                    if sigma < LM_MIN_SHIFT * cfg.K:
+                        sigma = 0.0
+    finally:
+        for h in damped.values():
+            h.close()
+    raise NonConvergence(f"STFAS (LM) cycle budget exhausted (residual {hist[-1][1]:.3e} > {tol:.3e})",
+                         residual=hist[-1][1], context=f"{budget} V-cycles")
+
+
+def _axpby_dev(y, x, a, b):
+    """y <- a x + b y on a (possibly strided-frame) contiguous slice."""
+    _lib.check(_lib.load().smk_axpby(_dev._DT[y.dtype], y.data_ptr(), x.data_ptr(), float(a), float(b), y.numel(),
+                                     _dev.stream()), "axpby")

@@ -281,3 +281,33 @@ def test_vcycle_graph_replay_and_recapture(nso):
     assert np.array_equal(flat(shared[0]), flat(own_a))
     assert np.array_equal(flat(shared[1]), flat(own_b))
     assert np.array_equal(flat(own_a), flat(direct_a))
+
+
+def test_solve_nso_lm_untriggered_equals_plain(nso):
+    """lm=True on a problem that converges: the shift never engages, the
+    iterates are the plain solve's (SPEC.md:351 'converge without LM')."""
+    pb = make_problem(2, n=8, N=4, seed=3)
+    s, cfg = spec_cfg(nso, pb)
+    a = nso.solve_nso(s, cfg, pb.v0, pb.vstar, eps=1e-9, cycle_budget=30, lm=True)
+    b = nso.solve_nso(s, cfg, pb.v0, pb.vstar, eps=1e-9, cycle_budget=30)
+    assert [c for c, _, _ in a.history] == [c for c, _, _ in b.history]
+    assert state_err(a.state, stfas.State(*b.state.numpy())) == 0.0
+
+
+def test_solve_nso_lm_shifted_path_matches_oracle(nso):
+    """Force the shifted (damped) cycles with a low stall threshold: every
+    cycle from the third on runs with K + sigma, sigma doubling.  Same
+    iterates and residual history as the oracle; the budget runs out on both
+    sides (NonConvergence here, converged=False there)."""
+    from paper_1608_01102_b200.errors import NonConvergence
+    pb = make_problem(2, n=8, N=4, seed=3)
+    s, cfg = spec_cfg(nso, pb)
+    ref = stfas.solve_nso_lm(pb, eps=1e-12, cycle_budget=7, stall=0.05)
+    assert not ref.converged
+    dev = nso.SpacetimeState.zeros(s, pb.N)
+    with pytest.raises(NonConvergence):
+        nso.solve_nso(s, cfg, pb.v0, pb.vstar, s=dev, eps=1e-12, cycle_budget=7, lm=True, lm_stall=0.05)
+    assert state_err(dev, ref.state, gauge=True) < 1e-8
+    # the shifted cycles still reduce the undamped residual
+    hist = [h[1] for h in ref.history]
+    assert hist[-1] < hist[2]

@@ -184,3 +184,18 @@ def test_vcycle_linear_convergence_small():
     # the 8^2 case coarsens to 4^2 (near-direct); mesh independence proper is
     # checked on the GPU at 16^2..32^2 (tests/test_gpu_convergence.py)
     assert max(facs) <= 0.75
+
+
+def test_lm_shift_keeps_the_fixed_point():
+    """oracle solve_nso_lm: with the shift forced on
+    it still converges to the undamped solution; untriggered it is the plain
+    solve."""
+    from problems import make_problem
+    pb = make_problem(2, n=8, N=4, seed=3)
+    plain = stfas.solve_nso(pb, eps=1e-9, cycle_budget=30)
+    lm = stfas.solve_nso_lm(pb, eps=1e-9, cycle_budget=30)
+    assert [h[1] for h in lm.history] == [h[1] for h in plain.history]
+    forced = stfas.solve_nso_lm(pb, eps=1e-9, cycle_budget=60, stall=0.3)
+    assert forced.converged
+    for a, b in zip(forced.state.V, plain.state.V):
+        assert np.max(np.abs(a - b)) <= 1e-6 * max(1.0, np.max(np.abs(b)))
