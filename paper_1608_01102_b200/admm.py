@@ -62,6 +62,7 @@ class ControlResult:
     state: SpacetimeState
     logs: list = field(default_factory=list)
     converged: bool = False
+    vcycle_log: list = field(default_factory=list)   # (admm_iter, vcycle_index, residual_inf, residual_l2, wall_ms)
 
     def write_log_csv(self, path):
         """Per-iteration CSV: outer_iter, ao_obj, nso_resid, visual_diff, wall_s."""
@@ -70,6 +71,15 @@ class ControlResult:
             w.writeheader()
             for row in self.logs:
                 w.writerow(row)
+
+    def write_vcycle_csv(self, path):
+        """nso_solver convergence rows: admm_iter, vcycle_index,
+        residual_inf, residual_l2, wall_ms (the solve's wall time averaged over
+        its V-cycles: the cycles run back to back on the device)."""
+        with open(path, "w", newline="") as f:
+            w = csv.writer(f)
+            w.writerow(["admm_iter", "vcycle_index", "residual_inf", "residual_l2", "wall_ms"])
+            w.writerows(self.vcycle_log)
 
 
 def objective(rho, keyframes, u, r):
@@ -118,6 +128,7 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
     ncfg = StfasConfig(dt=cfg.dt, K=cfg.K, r=cfg.r, n_levels=cfg.n_levels)
     hier = StfasHierarchy(spec, ncfg, n, dtype)
     logs = []
+    vlog = []
     result = None
     prev_aug = None
     t_start = time.perf_counter()
@@ -130,6 +141,7 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
                 ao_obj = _objective_dev(spec, vstar, guiding, keyframes, metric, aocfg, r0)
                 guide = tuple(_axpby(vc.clone(), lc, -1.0 / cfg.K, 1.0) for vc, lc in zip(vstar, lam))
                 hier.set_guide(v0, guide)
+                t_solve = time.perf_counter()
                 if cfg.lm:
                     hist = _solve_lm(spec, ncfg, hier, v0, guide, s, cfg.eps_stfas, cfg.relative_stfas,
                                      cfg.nso_cycle_budget)
@@ -140,6 +152,8 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
                 e.args = (f"outer iteration {it}: {e.args[0] if e.args else ''}",) + e.args[1:]
                 e.outer_iter = it
                 raise
+            per = (time.perf_counter() - t_solve) * 1e3 / max(1, len(hist) - 1)
+            vlog.extend((it, c, ri, r2, per if c else 0.0) for c, ri, r2 in hist)
             for k in range(spec.dim):
                 v[k][1:] = s.V[k][:n - 1]
             rho, _ = _rollout_dev(spec, vstar, r0, aocfg)
@@ -147,7 +161,7 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
             logs.append({"outer_iter": it, "ao_obj": ao_obj, "nso_resid": hist[-1][1], "visual_diff": diff,
                          "wall_s": time.perf_counter() - t_start})
             result = ControlResult(rho=rho, v=tuple(c.clone() for c in v), u=tuple(s.U), vstar=vstar,
-                                   lam=tuple(c.clone() for c in lam), state=s, logs=logs)
+                                   lam=tuple(c.clone() for c in lam), state=s, logs=logs, vcycle_log=vlog)
             if diff < eps_admm:
                 result.converged = True
                 return result

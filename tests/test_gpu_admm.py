@@ -71,6 +71,12 @@ def test_admm_converges_like_oracle(tmp_path):
     lines = path.read_text().splitlines()
     assert lines[0] == "outer_iter,ao_obj,nso_resid,visual_diff,wall_s"
     assert len(lines) == 1 + len(res.logs)
+    vpath = tmp_path / "vcycles.csv"
+    res.write_vcycle_csv(vpath)
+    rows = vpath.read_text().splitlines()
+    assert rows[0] == "admm_iter,vcycle_index,residual_inf,residual_l2,wall_ms"
+    assert {int(r.split(",")[0]) for r in rows[1:]} == {l["outer_iter"] for l in res.logs}
+    assert float(rows[-1].split(",")[2]) <= 1e-9
 
 
 def test_admm_max_iterations_with_multiplier_updates():
