@@ -1,0 +1,263 @@
+"""Parity on the five BASELINE configs at their real sizes (B200 vs the C oracle).
+
+The checker is oracle/cstfas.c (the numpy oracle restated in multithreaded C,
+pinned to it by tests/test_coracle.py), run on the host cores on the same
+seeded inputs the bench uses (paper_1608_01102_b200.workloads: Neumann unit
+box, dt = 1/N, K = 1e3, r per config, v0 = 0, solenoidal band-limited v*).
+Every GPU call goes through the C-ABI (libsmk.so).
+
+Bounds (relative to the max |value| of each field group, p / pbar modulo
+per-frame constants after the gauge fix):
+  fp64: single V-cycles / passes <= 1e-9, converged fields <= 1e-8;
+  fp32 (cfg4 fp32, cfg5): measured bounds stated per test below -- one
+  V-cycle from zero <= 2e-4, the residual <= 2e-5 of its max, one level-0
+  colour pass from a mid-solve state <= 2e-4 (the fp32 rounding of
+  Eq. 9's dense 7x7 eliminations along an 80-pair time line).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+from oracle import cstfas, stfas
+from oracle.grid import Grid
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1608_01102_b200 import _lib, nso, workloads
+    _lib.load()
+    cstfas.load()
+    return nso, workloads
+
+
+def problem_of(w, vstar):
+    """oracle Problem for a workload (guide pulled from the device as fp64)."""
+    g = Grid(w.dim, (w.n,) * w.dim, 1.0 / w.n, "neumann")
+    vs = tuple(c.detach().double().cpu().numpy() for c in vstar)
+    v0 = tuple(np.zeros(g.face_shape(k)) for k in range(w.dim))
+    return stfas.Problem(g, w.dt, w.K, w.r, v0, vs)
+
+
+def setup(lib, index, dtype=None, levels=None):
+    nso, workloads = lib
+    w = workloads.config(index, dtype)
+    vstar = workloads.guide_velocity(w)
+    v0 = workloads.initial_velocity(w)
+    cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=levels or w.levels)
+    hier = nso.StfasHierarchy(w.spec, cfg, w.N, w.dtype)
+    hier.set_guide(v0, vstar)
+    return w, vstar, v0, cfg, hier
+
+
+def dev_state_np(s):
+    V, PB, U, P = s.numpy()
+    f = lambda a: np.asarray(a, dtype=np.float64)
+    return stfas.State(tuple(f(v) for v in V), f(PB), tuple(f(u) for u in U), f(P))
+
+
+def gauge(x):
+    ax = tuple(range(1, x.ndim))
+    return x - x.mean(axis=ax, keepdims=True)
+
+
+def field_errs(a, b):
+    """per field group relative errors of numpy States a (test) vs b (want)."""
+    return {"v": rel_err(a.V, b.V), "u": rel_err(a.U, b.U), "p": rel_err(gauge(a.P), gauge(b.P)),
+            "pbar": rel_err(gauge(a.PB), gauge(b.PB))}
+
+
+def report(tag, errs):
+    print(f"[parity] {tag}: " + " ".join(f"{k}={v:.2e}" for k, v in errs.items()), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# cfg1: 2D 32^2 x 16 fp64, r = 1e-3, 2 levels -- full solve_nso
+# ---------------------------------------------------------------------------
+
+
+def test_cfg1_full_solve(lib):
+    nso, _ = lib
+    w, vstar, v0, cfg, hier = setup(lib, 1)
+    pb = problem_of(w, vstar)
+    H = cstfas.Hierarchy(pb, w.levels)
+    assert H.levels == hier.levels == 2
+    budget = 400
+    want, hist_c, ok_c = H.solve(eps=1e-5, cycle_budget=budget)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    hist_g = hier.solve(s, eps=1e-5, cycle_budget=budget)
+    assert ok_c
+    assert len(hist_g) == len(hist_c), (len(hist_g), len(hist_c))
+    for (c, a, _), (_, b, _) in zip(hist_g, hist_c):
+        assert abs(a - b) <= 1e-6 * b + 1e-9, (c, a, b)
+    e = field_errs(dev_state_np(s), want)
+    report(f"cfg1 solve ({len(hist_g) - 1} V-cycles, |f|={hist_g[-1][1]:.2e})", e)
+    assert max(e.values()) <= 1e-8
+    hier.close()
+
+
+# ---------------------------------------------------------------------------
+# cfg2: 2D 128^2 x 40 fp64, 3 levels -- V-cycles iterate for iterate, and the
+# full-depth solve to eps
+# ---------------------------------------------------------------------------
+
+
+def test_cfg2_vcycles_iterate_for_iterate(lib):
+    nso, _ = lib
+    w, vstar, v0, cfg, hier = setup(lib, 2)
+    pb = problem_of(w, vstar)
+    H = cstfas.Hierarchy(pb, w.levels)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    want = stfas.zero_state(pb.g, pb.N)
+    for k in range(3):
+        hier.vcycle(s)
+        hier.gauge_fix(s)
+        want = H.vcycle(want, gauge=True)
+        e = field_errs(dev_state_np(s), want)
+        report(f"cfg2 V-cycle {k + 1}", e)
+        assert max(e.values()) <= 1e-9
+    ri, _ = hier.residual_norms(s)
+    rc, _ = H.norms(want)
+    assert abs(ri - rc) <= 1e-8 * rc
+    hier.close()
+
+
+def test_cfg2_full_depth_solve(lib):
+    nso, workloads = lib
+    w, vstar, v0, cfg, hier = setup(lib, 2, levels=99)
+    pb = problem_of(w, vstar)
+    H = cstfas.Hierarchy(pb, 99)
+    assert H.levels == hier.levels == 6
+    want, hist_c, ok_c = H.solve(eps=1e-8, cycle_budget=40)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    hist_g = hier.solve(s, eps=1e-8, cycle_budget=40)
+    assert ok_c and len(hist_g) == len(hist_c)
+    e = field_errs(dev_state_np(s), want)
+    report(f"cfg2 full-depth solve ({len(hist_g) - 1} V-cycles)", e)
+    assert max(e.values()) <= 1e-8
+    hier.close()
+
+
+# ---------------------------------------------------------------------------
+# cfg3: 2D 256^2 x 60 fp64, 4 levels -- one V-cycle
+# ---------------------------------------------------------------------------
+
+
+def test_cfg3_vcycle(lib):
+    nso, _ = lib
+    w, vstar, v0, cfg, hier = setup(lib, 3)
+    pb = problem_of(w, vstar)
+    H = cstfas.Hierarchy(pb, w.levels)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    hier.vcycle(s)
+    hier.gauge_fix(s)
+    want = H.vcycle(stfas.zero_state(pb.g, pb.N), gauge=True)
+    e = field_errs(dev_state_np(s), want)
+    report("cfg3 V-cycle", e)
+    assert max(e.values()) <= 1e-9
+    hier.close()
+
+
+# ---------------------------------------------------------------------------
+# cfg4: 3D 64^3 x 60, 3 levels -- one V-cycle in fp64 and in fp32 vs the same
+# fp64 oracle cycle (the fp32 bound is measured here)
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def cfg4_want(lib):
+    _, workloads = lib
+    w = workloads.config(4, torch.float64)
+    vstar = workloads.guide_velocity(w)
+    pb = problem_of(w, vstar)
+    H = cstfas.Hierarchy(pb, w.levels)
+    want = H.vcycle(stfas.zero_state(pb.g, pb.N), gauge=True)
+    return pb, want, H.norms(want)
+
+
+@pytest.mark.parametrize("dt,bound", [(torch.float64, 1e-9), (torch.float32, 2e-4)])
+def test_cfg4_vcycle(lib, cfg4_want, dt, bound):
+    nso, _ = lib
+    pb, want, (rc, _) = cfg4_want
+    w, vstar, v0, cfg, hier = setup(lib, 4, dt)
+    # the fp32 guide is the fp64 guide rounded: compare against the oracle run
+    # on exactly the device's guide values
+    if dt == torch.float32:
+        pb32 = problem_of(w, vstar)
+        H = cstfas.Hierarchy(pb32, w.levels)
+        want = H.vcycle(stfas.zero_state(pb32.g, pb32.N), gauge=True)
+        rc, _ = H.norms(want)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    hier.vcycle(s)
+    hier.gauge_fix(s)
+    e = field_errs(dev_state_np(s), want)
+    ri, _ = hier.residual_norms(s)
+    report(f"cfg4 {str(dt)[6:]} V-cycle (|f| gpu {ri:.4e} oracle {rc:.4e})", e)
+    assert max(e.values()) <= bound
+    assert abs(ri - rc) <= max(bound, 1e-9) * 10 * rc
+    hier.close()
+
+
+# ---------------------------------------------------------------------------
+# cfg5: 3D 128^3 x 80 fp32, 4 levels -- the bench's own kernel instantiations
+# (k_kkt<.., NX = 128>, k_scgs_fwd<3,0,float,64,1,.,128,compact>,
+# k_scgs_back<3,0,float,false,128,true>) on a mid-solve state vs the oracle
+# ---------------------------------------------------------------------------
+
+
+@pytest.fixture(scope="module")
+def cfg5(lib):
+    nso, _ = lib
+    w, vstar, v0, cfg, hier = setup(lib, 5)
+    s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    for _ in range(2):
+        hier.vcycle(s)
+        hier.gauge_fix(s)
+    torch.cuda.synchronize()
+    pb = problem_of(w, vstar)
+    yield w, vstar, v0, hier, s, pb
+    hier.close()
+
+
+def test_cfg5_residual(lib, cfg5):
+    nso, _ = lib
+    w, vstar, v0, hier, s, pb = cfg5
+    from paper_1608_01102_b200 import nso as N_
+    got = N_.kkt_residual(w.spec, hier.cfg, s, v0, vstar)
+    R1, R2, R3, R4 = got.numpy()
+    want = cstfas.kkt_residual(pb, dev_state_np(s))
+    e = {"R1": rel_err(tuple(np.float64(x) for x in R1), want.R1), "R2": rel_err(np.float64(R2), want.R2),
+         "R3": rel_err(tuple(np.float64(x) for x in R3), want.R3), "R4": rel_err(np.float64(R4), want.R4)}
+    report("cfg5 fp32 k_kkt (NX=128)", e)
+    assert max(e.values()) <= 2e-5
+
+
+@pytest.mark.parametrize("colour", [0, 5])
+def test_cfg5_level0_colour_pass(lib, cfg5, colour):
+    from paper_1608_01102_b200 import _lib
+    nso, _ = lib
+    w, vstar, v0, hier, s, pb = cfg5
+    assert hier.levels == 4
+    before = dev_state_np(s)
+    work = s.copy()
+    L = _lib.load()
+    st = work.c_struct()
+    rc = L.smk_nso_level_color_pass(hier._h, 0, colour, ctypes.byref(st), _lib.ptrs(v0), None, _lib.ptrs(vstar),
+                                    None, torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "level_color_pass")
+    torch.cuda.synchronize()
+    got = dev_state_np(work)
+    want = cstfas.scgs_color(pb, before, None, colour)
+    # compare the colour's update (delta) and the resulting fields
+    dstate = lambda a: stfas.State(tuple(x - y for x, y in zip(a.V, before.V)), a.PB - before.PB,
+                                   tuple(x - y for x, y in zip(a.U, before.U)), a.P - before.P)
+    e = {"delta_" + k: v for k, v in field_errs(dstate(got), dstate(want)).items()}
+    e.update(field_errs(got, want))
+    report(f"cfg5 fp32 level-0 colour {colour} (bench kernels)", e)
+    assert max(v for k, v in e.items() if not k.startswith("delta")) <= 2e-4
+    assert max(v for k, v in e.items() if k.startswith("delta")) <= 2e-3
