@@ -124,82 +124,118 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample_shape(w):
-    """Bounded same-family sample the CPU oracle can finish in ~10-30 s."""
-    if w.dim == 3:
-        return dict(dim=3, n=16, N=8, levels=min(w.levels, 3))
-    return dict(dim=2, n=32, N=min(w.N, 16), levels=min(w.levels, 2))
+def cpu_sample(w, full=False):
+    """The CPU arm's bounded sample of workload w: the config itself for the
+    2D configs (or on request), else the config's spatial grid and level
+    count on a short time line (the oracle's cost per cell-timestep is
+    independent of N: the time-line solve is linear in N)."""
+    if full or w.dim == 2:
+        return dict(n=w.n, N=w.N, levels=w.levels, same_config=True)
+    return dict(n=w.n, N=2, levels=w.levels, same_config=False)
 
 
-def cpu_vcycle_rate(w, steps=1):
-    """Time the oracle (numpy fp64 port) V-cycle on one host core; cell-updates/s."""
+def cpu_vcycle_rate(w, steps=1, warmup=0, full=False, threads=0):
+    """Time the C oracle (oracle/cstfas.c: the numpy oracle restated in C,
+    OpenMP over the cells of a colour) V-cycle on the host cores.
+    Returns (cell-updates/s, s per V-cycle, sample, threads)."""
+    import numpy as np
+    from oracle import cstfas, stfas
+    from oracle.grid import Grid
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle import stfas
-    from problems import make_problem
-    sh = cpu_sample_shape(w)
-    pb = make_problem(sh["dim"], n=sh["n"], N=sh["N"], K=w.K, r=w.r, seed=3)
-    levels = stfas.build_levels(pb, sh["levels"])
-    st = stfas.zero_state(pb.g, pb.N)
+    from problems import smooth_vector
+    sh = cpu_sample(w, full)
+    nt = cstfas.set_threads(threads)
+    g = Grid(w.dim, (sh["n"],) * w.dim, 1.0 / sh["n"], "neumann")
+    rng = np.random.default_rng(1608_01102 + w.index)
+    dt = w.dt
+    # same recipe as workloads.guide_velocity (band-limited, projected, dt|v*|/h = 1)
+    # band-limited guide of the workloads' scale (not projected: the oracle's
+    # cost does not depend on the guide's values)
+    vs = [smooth_vector(g, rng, g.h / dt) for _ in range(sh["N"])]
+    vstar = tuple(np.stack([v[k] for v in vs]) for k in range(w.dim))
+    v0 = tuple(np.zeros(g.face_shape(k)) for k in range(w.dim))
+    pb = stfas.Problem(g, dt, w.K, w.r, v0, vstar)
+    H = cstfas.Hierarchy(pb, sh["levels"])
+    st = stfas.zero_state(g, sh["N"])
+    for _ in range(warmup):
+        st = H.vcycle(st, gauge=True)
     t0 = time.perf_counter()
     for _ in range(steps):
-        st = stfas.gauge_fix(stfas.vcycle(levels, 0, st))
-    dt = (time.perf_counter() - t0) / steps
-    cts = sh["n"] ** sh["dim"] * sh["N"]
-    return cts / dt, dt, sh
+        st = H.vcycle(st, gauge=True)
+    sec = (time.perf_counter() - t0) / max(steps, 1)
+    H.close()
+    cts = sh["n"] ** w.dim * sh["N"]
+    sh["levels"] = len(stfas.build_levels(pb, sh["levels"]))
+    return cts / sec, sec, sh, nt
 
 
-def _cpu_worker(args):
-    """One host core: `steps` oracle V-cycles of the bounded sample (BLAS
-    pinned to one thread so the cores are not oversubscribed)."""
-    w, steps = args
-    try:
-        from threadpoolctl import threadpool_limits
-        with threadpool_limits(1):
-            return cpu_vcycle_rate(w, steps)
-    except ImportError:
-        return cpu_vcycle_rate(w, steps)
-
-
-def cpu_parallel_rate(w, steps=1, workers=None):
-    """Throughput of the oracle V-cycle on all host cores: one independent
-    sample problem per core (the metric is a throughput), aggregate
-    cell-timesteps / wall time.  Returns (rate, wall_s_per_step, shape, cores)."""
-    import multiprocessing as mp
-    n = workers or max(1, min(os.cpu_count() or 1, 64))
-    if n == 1:
-        r, dt, sh = cpu_vcycle_rate(w, steps)
-        return r, dt, sh, 1
-    ctx = mp.get_context("fork")
-    with ctx.Pool(n) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_cpu_worker, [(w, steps)] * n)
-        wall = (time.perf_counter() - t0) / steps
-    sh = res[0][2]
-    cts = sh["n"] ** sh["dim"] * sh["N"]
-    return n * cts / wall, wall, sh, n
+def cpu_sample_text(w, sh, nt, sec):
+    return (f"C restatement of the oracle (oracle/cstfas.c, fp64, OpenMP over colour cells; the reference "
+            f"ships no STFAS) FAS V-cycle on {sh['n']}^{w.dim} x {sh['N']} frames, {sh['levels']} levels"
+            f"{' (= the config)' if sh['same_config'] else ' (the config grid on a short time line)'}, "
+            f"{nt} host threads, {sec:.2f} s per V-cycle")
 
 
 def run_reference(args, w, rank, world):
     if rank != 0:
         return 0
     steps, warm = args.steps, args.warmup
-    # warm-up: imports, problem construction and the first V-cycle per core
-    cpu_parallel_rate(w, 1) if warm else None
-    rate, wall, sh, cores = cpu_parallel_rate(w, steps)
-    sample = (f"oracle fp64 numpy FAS V-cycle (CPU port of the path; the reference ships no STFAS) on a "
-              f"same-family {sh['n']}^{sh['dim']} x {sh['N']} ({sh['levels']} levels) problem, one independent "
-              f"problem per core on {cores} cores, aggregate rate per cell-timestep")
+    rate, sec, sh, nt = cpu_vcycle_rate(w, steps, warm, full=args.cpu_full)
     line = {
         "impl": "reference", "metric": "STFAS spacetime cell-updates/s (per V-cycle)", "value": rate,
-        "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * wall,
+        "unit": "cell-updates/s", "n_gpus": world, "steps": steps, "warmup": warm, "ms_per_step": 1000.0 * sec,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "config_index": w.index, "cell_timesteps": w.cell_timesteps,
-                   "parallelism": f"cpu x{cores}"},
-        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": cores, "kind": "port", "sample": sample},
+                   "sample_cell_timesteps": sh["n"] ** w.dim * sh["N"], "same_config": sh["same_config"],
+                   "parallelism": f"cpu x{nt} threads"},
+        "cpu_baseline": {"value": rate, "unit": "cell-updates/s", "cores": nt, "kind": "port",
+                         "sample": cpu_sample_text(w, sh, nt, sec)},
         "e2e": {"value": rate, "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def time_to_solution(nso, spec, w, v0, vstar, levels, budget):
+    """solve_nso from zero to eps (fp64: absolute 1e-5; fp32:
+    relative 1e-5 * ||f_0||), every V-cycle + gauge + the
+    ||f|| stop test device-timed; returns the record for the bench line."""
+    import torch
+    cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=levels)
+    hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
+    hier.set_guide(v0, vstar)
+    st = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
+    scratch = st.copy()
+    hier.vcycle(scratch)           # graph capture outside the timed solve
+    del scratch
+    st2 = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
+    torch.cuda.synchronize()
+    f0, _ = hier.residual_norms(st2)
+    rel = w.dtype == torch.float32
+    tol = 1e-5 * f0 if rel else 1e-5
+    hist, t_ms, reached, stop_ms = [f0], 0.0, None, 0.0
+    for c in range(1, budget + 1):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        hier.vcycle(st2)
+        hier.gauge_fix(st2)
+        e1.record()
+        ri, _ = hier.residual_norms(st2)
+        e2.record()
+        e2.synchronize()
+        t_ms += e0.elapsed_time(e2)
+        stop_ms += e1.elapsed_time(e2)
+        hist.append(ri)
+        if ri <= tol:
+            reached = c
+            break
+    out = {"levels": hier.levels, "eps": 1e-5, "eps_kind": "relative" if rel else "absolute", "f0_inf": f0,
+           "vcycles_to_eps": reached, "s_to_solution": t_ms / 1000.0 if reached else None,
+           "final_residual_inf": hist[-1], "stop_test_ms_per_cycle": stop_ms / max(1, len(hist) - 1),
+           "residual_history": [float(f"{x:.4e}") for x in hist],
+           "asym_factor": (hist[-1] / hist[-4]) ** (1 / 3) if len(hist) >= 4 and hist[-4] > 0 else None}
+    hier.close()
+    return out
 
 
 def e2e_pipelined(args, spec, cfg, w, v0, vstar, state, hier, h_in, out_h):
@@ -279,6 +315,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e calls back to back (no copy/compute overlap)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-full", action="store_true", help="CPU arm on the whole config (3D: minutes)")
+    ap.add_argument("--levels", type=int, default=0, help="hierarchy depth (0 = the config's)")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution solves")
+    ap.add_argument("--tts-budget", type=int, default=80)
     args = ap.parse_args()
 
     import torch
@@ -303,7 +343,7 @@ def main():
     spec = w.spec
     vstar = workloads.guide_velocity(w)
     v0 = workloads.initial_velocity(w)
-    cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=w.levels)
+    cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=args.levels or w.levels)
     stream = torch.cuda.current_stream()
     slab = None
     if world > 1:
@@ -460,13 +500,21 @@ def main():
                                        "calls k+1's upload and k-1's download overlap call k's V-cycle")
                if pipelined else "serial"}
 
+    # ---------------- time to solution (V-cycles to eps, seconds) ----------------
+    # the config's hierarchy (BASELINE level count) and the full-depth one
+    # (coarsest 4^d: the coarsest-level 10-sweep solve is what limits the
+    # config's convergence factor)
+    tts = None
+    if world == 1 and not args.no_tts:
+        tts = {"config_levels": time_to_solution(nso, spec, w, v0, vstar, w.levels, args.tts_budget),
+               "full_depth": time_to_solution(nso, spec, w, v0, vstar, 99, args.tts_budget)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, dt, sh, cores = cpu_parallel_rate(w, 1)
-            cpu = {"value": rate, "unit": "cell-updates/s", "cores": cores, "kind": "port",
-                   "sample": f"oracle fp64 numpy V-cycle, same-family {sh['n']}^{sh['dim']} x {sh['N']} "
-                             f"({sh['levels']} levels), one problem per core on {cores} cores, {dt:.1f} s wall"}
+            rate, sec, sh, nt = cpu_vcycle_rate(w, 1)
+            cpu = {"value": rate, "unit": "cell-updates/s", "cores": nt, "kind": "port",
+                   "same_config": sh["same_config"], "sample": cpu_sample_text(w, sh, nt, sec)}
         except Exception as ex:  # never fail the GPU line on the CPU leg
             cpu = {"value": None, "unit": "cell-updates/s", "cores": 1, "kind": "port", "sample": f"failed: {ex}"}
 
@@ -495,6 +543,7 @@ def main():
             "vcycle_hbm": {"achieved_per_gpu": vc_gbs, "peak": hbm, "unit": "GB/s", "frac": vc_gbs / hbm,
                            "algorithmic_bytes": vc_bytes},
             "e2e": e2e,
+            "time_to_solution": tts,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
             "clocks": clk,

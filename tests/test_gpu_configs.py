@@ -10,9 +10,12 @@ Bounds (relative to the max |value| of each field group, p / pbar modulo
 per-frame constants after the gauge fix):
   fp64: single V-cycles / passes <= 1e-9, converged fields <= 1e-8;
   fp32 (cfg4 fp32, cfg5): measured bounds stated per test below -- one
-  V-cycle from zero <= 2e-4, the residual <= 2e-5 of its max, one level-0
-  colour pass from a mid-solve state <= 2e-4 (the fp32 rounding of
-  Eq. 9's dense 7x7 eliminations along an 80-pair time line).
+  V-cycle from zero <= 2e-4 (measured 7.4e-5 on pbar), the residual's
+  absolute error <= 1e-5 ||f_0||_inf (the fp32 stop test's scale; the rows
+  are differences of O(|u|/dt) terms, so relative-to-row bounds are
+  meaningless near convergence), one level-0 colour pass from a mid-solve
+  state <= 2e-4 (the fp32 rounding of Eq. 9's dense 7x7 eliminations along
+  an 80-pair time line).
 """
 
 import ctypes
@@ -215,33 +218,36 @@ def cfg5(lib):
     nso, _ = lib
     w, vstar, v0, cfg, hier = setup(lib, 5)
     s = nso.SpacetimeState.zeros(w.spec, w.N, w.dtype)
+    f0, _ = hier.residual_norms(s)
     for _ in range(2):
         hier.vcycle(s)
         hier.gauge_fix(s)
     torch.cuda.synchronize()
     pb = problem_of(w, vstar)
-    yield w, vstar, v0, hier, s, pb
+    yield w, vstar, v0, hier, s, pb, f0
     hier.close()
 
 
 def test_cfg5_residual(lib, cfg5):
     nso, _ = lib
-    w, vstar, v0, hier, s, pb = cfg5
+    w, vstar, v0, hier, s, pb, f0 = cfg5
     from paper_1608_01102_b200 import nso as N_
     got = N_.kkt_residual(w.spec, hier.cfg, s, v0, vstar)
     R1, R2, R3, R4 = got.numpy()
     want = cstfas.kkt_residual(pb, dev_state_np(s))
-    e = {"R1": rel_err(tuple(np.float64(x) for x in R1), want.R1), "R2": rel_err(np.float64(R2), want.R2),
-         "R3": rel_err(tuple(np.float64(x) for x in R3), want.R3), "R4": rel_err(np.float64(R4), want.R4)}
-    report("cfg5 fp32 k_kkt (NX=128)", e)
-    assert max(e.values()) <= 2e-5
+    # fp32 bound: the rows are differences of O(|u|/dt) terms, so the error is
+    # stated against the stop test's scale ||f_0||_inf (fp32 eps = 1e-5 ||f_0||)
+    ab = lambda a, b: max(float(np.max(np.abs(np.float64(x) - y))) for x, y in zip(a, b)) / f0
+    e = {"R1": ab(R1, want.R1), "R2": ab((R2,), (want.R2,)), "R3": ab(R3, want.R3), "R4": ab((R4,), (want.R4,))}
+    report(f"cfg5 fp32 k_kkt (NX=128), |err| / ||f0|| (||f0|| = {f0:.4g})", e)
+    assert max(e.values()) <= 1e-5
 
 
 @pytest.mark.parametrize("colour", [0, 5])
 def test_cfg5_level0_colour_pass(lib, cfg5, colour):
     from paper_1608_01102_b200 import _lib
     nso, _ = lib
-    w, vstar, v0, hier, s, pb = cfg5
+    w, vstar, v0, hier, s, pb, f0 = cfg5
     assert hier.levels == 4
     before = dev_state_np(s)
     work = s.copy()
