@@ -144,6 +144,8 @@ typedef struct smk_nso_params {
   int color_mod;  /* colouring modulus per axis (2: 4/8 colours) */
   int t0;         /* time-slab mode: global index of local pair 0 (0 otherwise) */
   int n_total;    /* time-slab mode: global pair count (0 = n_frames) */
+  int red_black;  /* != 0: 2 colours by (sum_k c_k) mod 2 (color_mod ignored);
+                     needs an even last-axis extent (periodic: even extents) */
 } smk_nso_params;
 
 /* Spacetime state (pair index i = 0..N-1): V[i]=v_{i+1}, PB[i]=pbar_{i+1},

@@ -72,6 +72,7 @@ typedef struct {
   const double* vstar[3];  /* vs_frames frames */
   int vs_frames;           /* N (v*_0..v*_{N-1}) or N+1 (slab mode) */
   const double* unext[3];  /* right halo (1 frame) or NULL */
+  int red_black;           /* 2 colours by parity of sum_k c_k (else mod-`colors`) */
 } cprob;
 
 /* ------------------------------------------------------------------ grid */
@@ -552,7 +553,12 @@ static int cell_line(const cprob* pb, const cstate* st, const cres* rhs, const c
   return ok;
 }
 
-static int color_of_cell(const cgrid* g, int mod, const int* c) {
+static int color_of_cell(const cgrid* g, int mod, int red_black, const int* c) {
+  if (red_black) {
+    int s = 0;
+    for (int k = 0; k < g->dim; ++k) s += c[k];
+    return s % 2;
+  }
   int col = 0, mul = 1;
   for (int k = 0; k < g->dim; ++k) {
     col += (c[k] % mod) * mul;
@@ -577,7 +583,7 @@ int cst_color_pass(const cprob* pb, cstate* st, const cres* rhs, int color, cons
     for (int64_t e = 0; e < nc; ++e) {
       int x[3];
       lat_coords(g, -1, e, x);
-      if (color_of_cell(g, pb->colors, x) == color) {
+      if (color_of_cell(g, pb->colors, pb->red_black, x) == color) {
         own[3 * M] = x[0];
         own[3 * M + 1] = x[1];
         own[3 * M + 2] = x[2];
@@ -647,6 +653,7 @@ int cst_color_pass(const cprob* pb, cstate* st, const cres* rhs, int color, cons
 int cst_sweep(const cprob* pb, cstate* st, const cres* rhs) {
   int nc = 1, rc = 0;
   for (int k = 0; k < pb->g.dim; ++k) nc *= pb->colors;
+  if (pb->red_black) nc = 2;
   for (int c = 0; c < nc; ++c) {
     int r = cst_color_pass(pb, st, rhs, c, NULL, 0, 1, NULL);
     if (r) rc = r;
@@ -659,6 +666,14 @@ int cst_sweep(const cprob* pb, cstate* st, const cres* rhs) {
 static int coarsenable(const cgrid* g) {
   for (int a = 0; a < g->dim; ++a)
     if (g->n[a] % 2 || g->n[a] / 2 < 4) return 0;
+  return 1;
+}
+/* oracle/stfas.py colourable: same-colour cells share no face */
+static int colourable(const cgrid* g, int mod, int red_black) {
+  for (int a = 0; a < g->dim; ++a) {
+    if (red_black && a == g->dim - 1 && g->n[a] % 2) return 0;
+    if (g->per && g->n[a] % (red_black ? 2 : mod)) return 0;
+  }
   return 1;
 }
 static cgrid coarse_of(const cgrid* g) {
@@ -841,6 +856,8 @@ chier* cst_hier_create(const cprob* top, int n_levels, int nu1, int nu2, int n_c
   const int N = top->N;
   res_alloc(&top->g, N, &H->lv[0].res);
   while (H->nl < n_levels && H->nl < 8 && coarsenable(&H->lv[H->nl - 1].pb.g)) {
+    cgrid gnext = coarse_of(&H->lv[H->nl - 1].pb.g);
+    if (!colourable(&gnext, top->colors, top->red_black)) break;
     clevel* f = &H->lv[H->nl - 1];
     clevel* c = &H->lv[H->nl];
     c->pb = f->pb;

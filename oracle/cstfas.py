@@ -42,7 +42,7 @@ class CProb(ctypes.Structure):
     _fields_ = [("g", CGrid), ("N", ctypes.c_int), ("dt", ctypes.c_double), ("K", ctypes.c_double),
                 ("r", ctypes.c_double), ("omega", ctypes.c_double), ("colors", ctypes.c_int),
                 ("t0", ctypes.c_int), ("Ng", ctypes.c_int), ("v0", _P * 3), ("vstar", _P * 3),
-                ("vs_frames", ctypes.c_int), ("unext", _P * 3)]
+                ("vs_frames", ctypes.c_int), ("unext", _P * 3), ("red_black", ctypes.c_int)]
 
 
 def build(force=False):
@@ -62,8 +62,8 @@ _lib = None
 def load():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB):
-            build()
+        if os.path.exists(SRC):
+            build()   # no-op when up to date (the GPU box has only the prebuilt .so)
         L = ctypes.CDLL(LIB)
         L.cst_hier_create.restype = ctypes.c_void_p
         L.cst_hier_create.argtypes = [ctypes.POINTER(CProb), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]
@@ -132,6 +132,7 @@ def _prob(pb, keep):
         if pb.unext is not None:
             c.unext[k] = keep.p(pb.unext[k])
     c.vs_frames = pb.vstar[0].shape[0]
+    c.red_black = 1 if pb.red_black else 0
     return c
 
 
@@ -201,7 +202,7 @@ def scgs_color(pb, st, rhs, color, cells=None, return_delta=False):
         keep.refs.append(c3)
         cptr, M = c3.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), c3.shape[0]
     else:
-        col = stfas.color_of(pb.g, pb.colors)
+        col = stfas.color_of(pb.g, pb.colors, pb.red_black)
         M = int(np.sum(col == color))
     b = 2 * pb.g.dim + 1
     x = np.zeros((M, 2 * pb.N, b))

@@ -87,7 +87,8 @@ class Problem:
     v0: tuple          # pinned initial velocity (face arrays)
     vstar: tuple       # (N, face) stacks: v*_0 .. v*_{N-1}
     omega: float = 0.8
-    colors: int = 2    # colouring modulus per axis (2 -> 2^d colours)
+    colors: int = 2    # colouring modulus per axis (2 -> 2^d colours), when not red-black
+    red_black: bool = True   # 2 colours by (sum_k c_k) mod 2
     # time-slab mode: local pairs t0 .. t0+n_pairs-1 of Ng;
     # v0 is the left halo, unext the right halo u_{t0+n_pairs}, vstar holds
     # n_pairs + 1 frames (v*_{t0} .. v*_{t0+n_pairs})
@@ -159,9 +160,11 @@ def kkt_residual(pb, st):
 # ---------------------------------------------------------------------------
 
 
-def color_of(g, mod=2):
-    """Colour id per cell: sum_k (c_k mod m) m^k."""
+def color_of(g, mod=2, red_black=False):
+    """Colour id per cell: red-black (sum_k c_k) mod 2, else sum_k (c_k mod m) m^k."""
     idx = np.indices(g.res)
+    if red_black:
+        return np.sum(idx, axis=0) % 2
     col = np.zeros(g.res, dtype=np.int64)
     mul = 1
     for k in range(g.dim):
@@ -170,8 +173,18 @@ def color_of(g, mod=2):
     return col
 
 
-def n_colors(g, mod=2):
-    return mod ** g.dim
+def n_colors(g, mod=2, red_black=False):
+    return 2 if red_black else mod ** g.dim
+
+
+def colourable(g, mod=2, red_black=False):
+    """Same-colour cells must not share a face: red-black needs
+    an even last-axis extent (equal colour rows) and, periodic, even extents
+    (the wrap neighbour has the other parity); mod-m colouring of a periodic
+    grid needs every extent divisible by m."""
+    if red_black:
+        return g.res[-1] % 2 == 0 and (not g.periodic or all(r % 2 == 0 for r in g.res))
+    return not g.periodic or all(r % mod == 0 for r in g.res)
 
 
 class CellSlots:
@@ -335,7 +348,7 @@ def scgs_color(pb, st, rhs, color, cells=None, return_delta=False):
     """One colour pass (snapshot reads, in-colour Jacobi); returns new State."""
     g = pb.g
     if cells is None:
-        col = color_of(g, pb.colors)
+        col = color_of(g, pb.colors, pb.red_black)
         cells = np.argwhere(col == color)
     slots = CellSlots(g, cells)
     N, nf = pb.N, 2 * g.dim
@@ -357,7 +370,7 @@ def scgs_color(pb, st, rhs, color, cells=None, return_delta=False):
 
 def scgs_smooth(pb, st, rhs=None):
     """One full sweep over all colours."""
-    for c in range(n_colors(pb.g, pb.colors)):
+    for c in range(n_colors(pb.g, pb.colors, pb.red_black)):
         st = scgs_color(pb, st, rhs, c)
     return st
 
@@ -388,12 +401,12 @@ def build_levels(pb, n_levels):
     while len(levels) < n_levels:
         top = levels[-1]
         gc = top.g.coarsen()
-        if gc is None:
+        if gc is None or not colourable(gc, top.colors, top.red_black):
             break
         levels.append(Problem(gc, top.dt, top.K, top.r,
                               ops.restrict_face(top.g, top.v0),
                               ops.restrict_face(top.g, top.vstar),
-                              top.omega, top.colors))
+                              top.omega, top.colors, top.red_black))
     return levels
 
 

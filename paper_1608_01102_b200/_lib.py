@@ -35,7 +35,8 @@ class smk_nso_params(ctypes.Structure):
     _fields_ = [("n_frames", ctypes.c_int), ("n_levels", ctypes.c_int), ("dt", ctypes.c_double),
                 ("K", ctypes.c_double), ("r", ctypes.c_double), ("omega", ctypes.c_double),
                 ("nu1", ctypes.c_int), ("nu2", ctypes.c_int), ("n_coarse", ctypes.c_int),
-                ("color_mod", ctypes.c_int), ("t0", ctypes.c_int), ("n_total", ctypes.c_int)]
+                ("color_mod", ctypes.c_int), ("t0", ctypes.c_int), ("n_total", ctypes.c_int),
+                ("red_black", ctypes.c_int)]
 
 
 VP3 = ctypes.c_void_p * 3

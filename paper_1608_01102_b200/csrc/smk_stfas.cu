@@ -382,6 +382,31 @@ struct Slots {
   static constexpr int C = NF + 1;  // W columns (faces) + z
 };
 
+// Colour cell m -> cell coordinates.  mod > 0: mod-m colouring, colour
+// digits (o0, o1, o2), cells o_a + mod * q_a; mod < 0: red-black, colour o0,
+// cells with (sum_a c_a) % 2 == o0 -- unit stride on the leading axes, stride
+// 2 along the last axis starting at the row's parity (even last extent, so
+// every row holds m_last colour cells).
+template <int DIM>
+__device__ __forceinline__ void color_cell(int64_t m, int o0, int o1, int o2, int mod, int m1, int m2, int (&c)[3]) {
+  int64_t q = m;
+  const int q2 = (int)(q % m2); q /= m2;
+  const int q1 = (int)(q % m1); q /= m1;
+  if (mod > 0) {
+    c[0] = o0 + mod * (int)q;
+    c[1] = o1 + mod * q1;
+    c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+  } else if (DIM == 3) {
+    c[0] = (int)q;
+    c[1] = q1;
+    c[2] = ((o0 + c[0] + c[1]) & 1) + 2 * q2;
+  } else {
+    c[0] = (int)q;
+    c[1] = ((o0 + c[0]) & 1) + 2 * q1;
+    c[2] = 0;
+  }
+}
+
 // colour-cell geometry shared by the smoother kernels
 template <int DIM, bool PER, class R>
 struct CellGeo {
@@ -392,12 +417,7 @@ struct CellGeo {
   R gcol[NF];
   __device__ __forceinline__ CellGeo(const Ix<DIM, PER>& ix, R h, int64_t m, int o0, int o1, int o2, int mod, int m1,
                                      int m2) {
-    int64_t q = m;
-    int q2 = (int)(q % m2); q /= m2;
-    int q1 = (int)(q % m1); q /= m1;
-    c[0] = o0 + mod * (int)q;
-    c[1] = o1 + mod * q1;
-    c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+    color_cell<DIM>(m, o0, o1, o2, mod, m1, m2, c);
 #pragma unroll
     for (int k = 0; k < DIM; ++k)
 #pragma unroll
@@ -1281,12 +1301,7 @@ __global__ void __launch_bounds__(256) k_scgs_apply(Ix<DIM, PER> ix, StP<R> s, i
   const int fstride = gridDim.z;
   SMK_FRAME_LOOP(m, M) {
     int c[3];
-    int q = m;
-    int q2 = q % m2; q /= m2;
-    int q1 = q % m1; q /= m1;
-    c[0] = o0 + mod * q;
-    c[1] = o1 + mod * q1;
-    c[2] = DIM == 3 ? o2 + mod * q2 : 0;
+    color_cell<DIM>(m, o0, o1, o2, mod, m1, m2, c);
     int64_t fo[NF];
     bool w[NF];
 #pragma unroll
@@ -1460,7 +1475,7 @@ struct Nso : NsoBase {
       L.nc = cells_of(cur);
       for (int k = 0; k < DIM; ++k) L.nf[k] = faces_of(cur, k);
       lv.push_back(L);
-      if (!can_coarsen(cur)) break;
+      if (!can_coarsen(cur) || !colourable(coarsen(cur))) break;
       cur = coarsen(cur);
     }
     const int N = p.n_frames;
@@ -1482,8 +1497,12 @@ struct Nso : NsoBase {
       }
       face_alloc(L.f.R1, N); L.f.R2 = alloc((int64_t)N * L.nc);
       face_alloc(L.f.R3, N); L.f.R4 = alloc((int64_t)N * L.nc);
-      int64_t M = 1;
-      for (int a = 0; a < DIM; ++a) M *= (L.g.n[a] + p.color_mod - 1) / p.color_mod;
+      int o[3], mm[3];
+      int64_t M = 0;
+      for (int col = 0; col < n_colors(); ++col) {
+        const int64_t Mc = color_geometry(L.g, col, o, mm);
+        M = Mc > M ? Mc : M;
+      }
       maxM = M > maxM ? M : maxM;
     }
     constexpr int B = Slots<DIM>::B;
@@ -1594,10 +1613,43 @@ struct Nso : NsoBase {
   }
 
   int n_colors() const {
+    if (prm.red_black) return 2;
     int ncol = 1;
     for (int a = 0; a < DIM; ++a) ncol *= prm.color_mod;
     return ncol;
   }
+  // colouring validity: same-colour cells must
+  // not share a face -- red-black needs an even last-axis extent (and even
+  // periodic extents: the wrap neighbour has the other parity); mod-m needs
+  // periodic extents divisible by m
+  bool colourable(const Geo& g) const {
+    for (int a = 0; a < DIM; ++a) {
+      if (prm.red_black && a == DIM - 1 && g.n[a] % 2) return false;
+      if (PER && g.n[a] % (prm.red_black ? 2 : prm.color_mod)) return false;
+    }
+    return true;
+  }
+  // kernel colour geometry (color_cell): offsets o, extents mm, the kernels'
+  // mod argument (-1 = red-black); returns the colour's cell count
+  int64_t color_geometry(const Geo& g, int col, int (&o)[3], int (&mm)[3]) const {
+    o[0] = o[1] = o[2] = 0;
+    mm[0] = mm[1] = mm[2] = 1;
+    if (prm.red_black) {
+      o[0] = col;
+      for (int a = 0; a < DIM; ++a) mm[a] = a == DIM - 1 ? g.n[a] / 2 : g.n[a];
+    } else {
+      const int mod = prm.color_mod;
+      int cc = col;
+      for (int a = 0; a < DIM; ++a) {
+        o[a] = cc % mod;
+        cc /= mod;
+        mm[a] = (g.n[a] - o[a] + mod - 1) / mod;
+        if (mm[a] < 0) mm[a] = 0;
+      }
+    }
+    return (int64_t)mm[0] * mm[1] * mm[2];
+  }
+  int kernel_mod() const { return prm.red_black ? -1 : prm.color_mod; }
 
   void sweep(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
@@ -1643,19 +1695,12 @@ struct Nso : NsoBase {
 
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
     const Level<R>& L = lv[l];
-    const int mod = prm.color_mod;
+    const int mod = kernel_mod();
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     Ix<DIM, PER> ix(L.g);
-    int o[3] = {0, 0, 0}, mm[3] = {1, 1, 1};
-    int cc = col;
-    for (int a = 0; a < DIM; ++a) {
-      o[a] = cc % mod;
-      cc /= mod;
-      mm[a] = (L.g.n[a] - o[a] + mod - 1) / mod;
-      if (mm[a] < 0) mm[a] = 0;
-    }
-    int64_t M = (int64_t)mm[0] * mm[1] * mm[2];
+    int o[3], mm[3];
+    const int64_t M = color_geometry(L.g, col, o, mm);
     if (M == 0) return;
     // forward: TM colour cells per CTA (producer + consumer warp per 32);
     // small colours use TM = 32 to spread over all SMs
@@ -2002,8 +2047,25 @@ static int check_params(const smk_nso_params* p) {
   }
   if (p->n_frames < 1) { set_error("n_frames must be >= 1"); return SMK_ERR_ARG; }
   if (!(p->dt > 0) || !(p->r > 0) || !(p->K >= 0)) { set_error("dt, r must be positive, K >= 0"); return SMK_ERR_ARG; }
-  if (p->color_mod < 2) { set_error("color_mod must be >= 2"); return SMK_ERR_ARG; }
+  if (!p->red_black && p->color_mod < 2) { set_error("color_mod must be >= 2"); return SMK_ERR_ARG; }
   if (p->nu1 < 0 || p->nu2 < 0 || p->n_coarse < 0) { set_error("negative sweep counts"); return SMK_ERR_ARG; }
+  return SMK_OK;
+}
+
+// the colouring must keep same-colour cells face-disjoint on the top level
+// (coarser levels stop before a level that breaks it, Nso::colourable)
+static int check_colouring(const smk_grid* g, const smk_nso_params* p) {
+  const int mod = p->red_black ? 2 : p->color_mod;
+  for (int a = 0; a < g->dim; ++a) {
+    if (p->red_black && a == g->dim - 1 && g->res[a] % 2) {
+      set_error("red-black colouring needs an even extent along the last axis");
+      return SMK_ERR_ARG;
+    }
+    if (g->boundary == SMK_PERIODIC && g->res[a] % mod) {
+      set_error("periodic extents must be divisible by the colouring modulus (%d)", mod);
+      return SMK_ERR_ARG;
+    }
+  }
   return SMK_OK;
 }
 
@@ -2027,7 +2089,7 @@ static NsoBase* make_nso(const smk_grid* g, const smk_nso_params* p) {
 extern "C" {
 
 smk_nso* smk_nso_create(const smk_grid* g, const smk_nso_params* p) {
-  if (check_grid(g) || check_params(p)) return nullptr;
+  if (check_grid(g) || check_params(p) || check_colouring(g, p)) return nullptr;
   NsoBase* impl = make_nso<int>(g, p);
   if (!impl) return nullptr;
   smk_nso* h = new smk_nso;
@@ -2151,7 +2213,7 @@ int smk_kkt_residual(const smk_grid* g, const smk_nso_params* p, const smk_state
 
 int smk_scgs_sweep(const smk_grid* g, const smk_nso_params* p, const smk_state* s, const void* const v0[],
                    const void* const vstar[], const smk_residual* rhs, void* stream) {
-  if (check_grid(g) || check_params(p)) return SMK_ERR_ARG;
+  if (check_grid(g) || check_params(p) || check_colouring(g, p)) return SMK_ERR_ARG;
   smk_nso_params q = *p;
   q.n_levels = 1;
   return dispatch(g, [&](auto tag) {

@@ -34,7 +34,8 @@ class StfasConfig:
     nu1: int = 2                # pre-smoothing (Alg. 2 line PRE)
     nu2: int = 2                # post-smoothing
     n_coarse: int = 10          # coarsest sweeps (Alg. 2 line FINAL)
-    color_mod: int = 2          # 4 colours (2D) / 8 colours (3D)
+    color_mod: int = 2          # mod-m colouring when not red-black: 4 colours (2D) / 8 colours (3D)
+    red_black: bool = True      # 2 colours by (sum_k c_k) mod 2
     n_levels: int = 99          # clipped to the grid's coarsening chain
 
     def params(self, N, t0=0, n_total=0):
@@ -49,6 +50,7 @@ class StfasConfig:
         p.omega = float(self.omega)
         p.nu1, p.nu2, p.n_coarse = int(self.nu1), int(self.nu2), int(self.n_coarse)
         p.color_mod = int(self.color_mod)
+        p.red_black = 1 if self.red_black else 0
         return p
 
 

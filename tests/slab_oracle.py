@@ -6,17 +6,24 @@ from oracle import ops, stfas
 
 
 class OracleEngine:
-    def __init__(self, g, dt, K, r, t0, t1, n_total, n_levels, omega=0.8, colors=2):
-        self.grids = g.hierarchy(n_levels)
+    def __init__(self, g, dt, K, r, t0, t1, n_total, n_levels, omega=0.8, colors=2, red_black=True):
+        self.grids = [gg for gg in g.hierarchy(n_levels)]
+        keep = [self.grids[0]]
+        for gg in self.grids[1:]:
+            if not stfas.colourable(gg, colors, red_black):
+                break
+            keep.append(gg)
+        self.grids = keep
         self.n_levels = len(self.grids)
         self.dt, self.K, self.r, self.omega, self.colors = dt, K, r, omega, colors
+        self.red_black = red_black
         self.t0, self.t1, self.Nl, self.Ng = t0, t1, t1 - t0, n_total
-        self.n_colors = colors ** g.dim
+        self.n_colors = stfas.n_colors(g, colors, red_black)
 
     def _pb(self, l, halo):
         g = self.grids[l]
         return stfas.Problem(g, self.dt, self.K, self.r, halo.vprev, halo.vs, self.omega, self.colors,
-                             t0=self.t0, Ng=self.Ng, n_pairs=self.Nl, unext=halo.unext)
+                             self.red_black, t0=self.t0, Ng=self.Ng, n_pairs=self.Nl, unext=halo.unext)
 
     def halo_buffers(self, l):
         g = self.grids[l]
@@ -88,7 +95,7 @@ def build_oracle_solver(pb, n_levels, slab_ids, n_slabs, comm=None):
     engines, guides = [], []
     for p in slab_ids:
         t0, t1 = ranges[p]
-        e = OracleEngine(pb.g, pb.dt, pb.K, pb.r, t0, t1, N, n_levels, pb.omega, pb.colors)
+        e = OracleEngine(pb.g, pb.dt, pb.K, pb.r, t0, t1, N, n_levels, pb.omega, pb.colors, pb.red_black)
         vs = []
         for c in pb.vstar:
             pad = np.zeros((max(0, t1 + 1 - N),) + c.shape[1:])

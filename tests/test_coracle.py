@@ -40,13 +40,15 @@ def test_kkt_residual_matches_numpy_oracle(dim, n, N, bnd):
     assert _res_err(cstfas.kkt_residual(pb, st, rhs), stfas.kkt_residual(pb, st).sub(rhs)) <= 1e-14
 
 
+@pytest.mark.parametrize("rb", [True, False])
 @pytest.mark.parametrize("dim,n,N,bnd", CASES)
-def test_colour_pass_matches_numpy_oracle(dim, n, N, bnd):
+def test_colour_pass_matches_numpy_oracle(dim, n, N, bnd, rb):
     pb = make_problem(dim, n=n, N=N, boundary=bnd, seed=4)
+    pb.red_black = rb
     rng = np.random.default_rng(2)
     st = random_state(pb, rng, 0.1)
     rhs = random_residual(pb, rng, 0.1)
-    for colour in (0, 3):
+    for colour in ((0, 1) if rb else (0, 3)):
         a, xa = stfas.scgs_color(pb, st, rhs, colour, return_delta=True)
         b, xb = cstfas.scgs_color(pb, st, rhs, colour, return_delta=True)
         assert rel_err(xb, xa) <= 1e-10
@@ -56,7 +58,7 @@ def test_colour_pass_matches_numpy_oracle(dim, n, N, bnd):
 def test_colour_pass_cell_subset_and_order():
     pb = make_problem(2, n=8, N=3, seed=6)
     st = random_state(pb, np.random.default_rng(6), 0.1)
-    cells = np.argwhere(stfas.color_of(pb.g) == 1)
+    cells = np.argwhere(stfas.color_of(pb.g, 2, pb.red_black) == 1)
     a, xa = cstfas.scgs_color(pb, st, None, 1, cells=cells, return_delta=True)
     b, xb = cstfas.scgs_color(pb, st, None, 1, cells=cells[::-1].copy(), return_delta=True)
     assert np.array_equal(xa, xb[::-1]) and _st_err(a, b) == 0.0
@@ -93,10 +95,11 @@ def test_transfers_match_numpy_oracle_bitwise():
         assert all(np.array_equal(a, b) for a, b in zip(ff, ops.prolong_face(gc, fc)))
 
 
-@pytest.mark.parametrize("dim,n,N,bnd,lv", [(2, 16, 4, "neumann", 2), (2, 16, 4, "periodic", 3),
-                                            (3, 8, 2, "neumann", 2)])
-def test_vcycle_matches_numpy_oracle(dim, n, N, bnd, lv):
+@pytest.mark.parametrize("dim,n,N,bnd,lv,rb", [(2, 16, 4, "neumann", 2, True), (2, 16, 4, "periodic", 3, True),
+                                               (3, 8, 2, "neumann", 2, True), (2, 16, 4, "neumann", 3, False)])
+def test_vcycle_matches_numpy_oracle(dim, n, N, bnd, lv, rb):
     pb = make_problem(dim, n=n, N=N, boundary=bnd, seed=3)
+    pb.red_black = rb
     levels = stfas.build_levels(pb, lv)
     H = cstfas.Hierarchy(pb, lv)
     assert H.levels == len(levels)
