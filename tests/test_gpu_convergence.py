@@ -66,22 +66,24 @@ def test_converged_solution_matches_oracle(bnd):
 
 
 def test_colour_order_converges_to_same_solution():
-    """north_star: colouring differences (mod-2 vs mod-3) converge to the same
-    solution within tolerance."""
+    """north_star: colouring differences (red-black vs mod-2 vs mod-3)
+    converge to the same solution within tolerance."""
     from paper_1608_01102_b200 import nso
     from paper_1608_01102_b200.fields import GridSpec
     pb = make_problem(2, n=24, N=4, seed=71, res=(24, 24))
     g = pb.g
     spec = GridSpec(g.dim, g.res, g.h, g.boundary)
     out = []
-    for mod in (2, 3):
-        r = nso.solve_nso(spec, nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, color_mod=mod, n_levels=3),
+    for rb, mod in ((True, 2), (False, 2), (False, 3)):
+        r = nso.solve_nso(spec, nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, color_mod=mod, red_black=rb,
+                                                n_levels=3),
                           pb.v0, pb.vstar, eps=1e-11, cycle_budget=80)
         out.append(r.state.numpy())
-    a, b = out
+    a = out[0]
     scale = max(np.max(np.abs(c)) for c in a[0] + a[2])
-    err = max(np.max(np.abs(x - y)) for x, y in zip(a[0] + a[2], b[0] + b[2]))
-    assert err <= 1e-8 * scale
+    for b in out[1:]:
+        err = max(np.max(np.abs(x - y)) for x, y in zip(a[0] + a[2], b[0] + b[2]))
+        assert err <= 1e-8 * scale
 
 
 def test_fp32_solution_bound():

@@ -29,7 +29,8 @@ def spec_cfg(nso, pb, **kw):
     from paper_1608_01102_b200.fields import GridSpec
     g = pb.g
     s = GridSpec(g.dim, g.res, g.h, g.boundary)
-    cfg = nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, omega=pb.omega, color_mod=pb.colors, **kw)
+    cfg = nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, omega=pb.omega, color_mod=pb.colors,
+                          red_black=pb.red_black, **kw)
     return s, cfg
 
 
@@ -175,12 +176,14 @@ def shape_env(monkeypatch):
 BACKS = {"flat": (0, 1), "pipe": (1 << 40, 0), "deep": (1 << 40, 1)}
 
 
+@pytest.mark.parametrize("rb", [True, False])
 @pytest.mark.parametrize("fwd", list(SHAPES))
 @pytest.mark.parametrize("back", list(BACKS))
 @pytest.mark.parametrize("dim,bnd", [(2, "neumann"), (3, "neumann"), (3, "periodic")])
-def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back, dim, bnd):
+def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back, dim, bnd, rb):
     shape_env(fwd, *BACKS[back])
     pb = make_problem(dim, n=8, N=5, boundary=bnd, seed=23)
+    pb.red_black = rb
     rng = np.random.default_rng(7)
     st = random_state(pb, rng, 0.05)
     rhs = random_residual(pb, rng, 0.05)
@@ -209,7 +212,7 @@ def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
     from paper_1608_01102_b200.fields import GridSpec
     n, N = 64, 6
     spec = GridSpec(3, (n, n, n), 1.0 / n, "neumann")
-    cfg = nso.StfasConfig(dt=1.0 / N, K=1e3, r=1e3, omega=0.8, color_mod=2)
+    cfg = nso.StfasConfig(dt=1.0 / N, K=1e3, r=1e3, omega=0.8)
     g = torch.Generator().manual_seed(5)
     shp = lambda k: (N,) + tuple(n + (a == k) for a in range(3))
     V = tuple((0.1 * torch.randn(shp(k), generator=g, dtype=torch.float64)) for k in range(3))

@@ -19,12 +19,12 @@ import torch  # noqa: E402
 from paper_1608_01102_b200 import nso, workloads  # noqa: E402
 
 
-def run(w, levels, n_coarse, budget, eps_rel, nu=(2, 2), color_mod=2, omega=0.8):
+def run(w, levels, n_coarse, budget, eps_rel, nu=(2, 2), color_mod=2, omega=0.8, red_black=True):
     spec = w.spec
     vstar = workloads.guide_velocity(w)
     v0 = workloads.initial_velocity(w)
     cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=levels, n_coarse=n_coarse, nu1=nu[0], nu2=nu[1],
-                          color_mod=color_mod, omega=omega)
+                          color_mod=color_mod, omega=omega, red_black=red_black)
     hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
     hier.set_guide(v0, vstar)
     st = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
@@ -57,7 +57,7 @@ def run(w, levels, n_coarse, budget, eps_rel, nu=(2, 2), color_mod=2, omega=0.8)
     tail = facs[-5:]
     asym = (hist[-1][1] / hist[-1 - len(tail)][1]) ** (1.0 / len(tail)) if tail else None
     out = {"config": w.index, "dtype": str(w.dtype).replace("torch.", ""), "levels": hier.levels,
-           "n_coarse": n_coarse, "nu": list(nu), "color_mod": color_mod, "omega": omega,
+           "n_coarse": n_coarse, "nu": list(nu), "color_mod": color_mod, "red_black": red_black, "omega": omega,
            "f0_inf": f0, "eps_rel": eps_rel, "vcycles_to_eps": reached[0] if reached else None,
            "s_to_solution": reached[1] / 1000.0 if reached else None,
            "ms_per_cycle_incl_stop": t_tot / max(1, len(hist) - 1), "asym_factor": asym,
@@ -76,6 +76,7 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-5)
     ap.add_argument("--color-mod", type=int, default=2)
     ap.add_argument("--omega", type=float, default=0.8)
+    ap.add_argument("--mod", action="store_true", help="mod-m colouring instead of red-black")
     a = ap.parse_args()
     dt = {"fp32": torch.float32, "fp64": torch.float64}.get(a.dtype)
     for ci in a.config:
@@ -83,7 +84,8 @@ def main():
         for lv in a.levels:
             for nc in a.n_coarse:
                 t = time.time()
-                o = run(w, lv if lv > 0 else w.levels, nc, a.budget, a.eps, color_mod=a.color_mod, omega=a.omega)
+                o = run(w, lv if lv > 0 else w.levels, nc, a.budget, a.eps, color_mod=a.color_mod, omega=a.omega,
+                        red_black=not a.mod)
                 o["wall_s"] = time.time() - t
                 print(json.dumps(o), flush=True)
 
