@@ -62,6 +62,9 @@ const char* smk_last_error(void);
 int smk_version(void);
 /* number of kernels the library has launched in this process (accounting) */
 long long smk_launch_count(void);
+/* release the operator scratch pool (stream-ordered buffers the raw operators
+ * reuse across calls, keyed by device, <= 4 GiB pooled per device) */
+void smk_pool_trim(void);
 
 /* ---------------- field core (fields.py) ---------------- */
 
@@ -183,6 +186,9 @@ int64_t smk_nso_device_bytes(const smk_nso* h);
 /* Bind the (device) v0 / vstar of the top level; restricts them down the
  * hierarchy.  Must be called before vcycle/solve and again when they change. */
 int smk_nso_set_guide(smk_nso* h, const void* const v0[], const void* const vstar[], void* stream);
+/* Update K on an existing hierarchy (the LM proximal shift);
+ * the next V-cycle re-captures its graph. */
+int smk_nso_set_K(smk_nso* h, double K);
 /* One FAS V(nu1, nu2) cycle (PAPER Alg. 2) on the caller's top-level state. */
 int smk_nso_vcycle(smk_nso* h, const smk_state* s, void* stream);
 /* ||f||_inf and ||f||_2 of the top level (synchronising). */

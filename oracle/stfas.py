@@ -467,16 +467,17 @@ def solve_nso(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None,
     return NsoResult(st, hist, False)
 
 
-LM_WINDOW, LM_STALL, LM_MIN_SHIFT = 3, 0.95, 1e-3
+LM_WINDOW, LM_STALL, LM_MIN_SHIFT, LM_MAX_SHIFT = 3, 0.95, 1e-3, 1e3
 
 
 def solve_nso_lm(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None, stall=LM_STALL):
     """SPEC.md:347 LM safeguard as frozen in DESIGN §11 (proximal shift):
-    while the per-cycle reduction factor over 3 cycles exceeds 0.95 the K/r
-    blocks get a shift sigma (K, doubled while stalled, halved while
-    progressing, dropped below 1e-3 K); a shifted V-cycle solves the problem
-    with K + sigma and guide (K v* + sigma v^k)/(K + sigma).  The stop test
-    uses the undamped residual."""
+    the per-cycle reduction factor over the last 3 cycles is tested only
+    once 3 cycles have run since the last change of sigma; if it exceeds 0.95
+    the K/r blocks get a shift sigma (K, then doubled, capped at 1e3 K), while
+    progressing it is halved and dropped below 1e-3 K.  A shifted V-cycle
+    solves the problem with K + sigma and guide (K v* + sigma v^k)/(K + sigma).
+    The stop test uses the undamped residual."""
     import dataclasses
     levels = build_levels(pb, n_levels if n_levels else 99)
     if st is None:
@@ -486,7 +487,7 @@ def solve_nso_lm(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None, stall=LM
     hist = [(0, r.inf(), r.l2())]
     if hist[0][1] <= eps:
         return NsoResult(st, hist, True)
-    sigma = 0.0
+    sigma, changed = 0.0, 0
     for c in range(1, cycle_budget + 1):
         if sigma > 0:
             K2 = pb.K + sigma
@@ -503,13 +504,16 @@ def solve_nso_lm(pb, st=None, eps=1e-5, cycle_budget=50, n_levels=None, stall=LM
         hist.append((c, r.inf(), r.l2()))
         if r.inf() <= eps:
             return NsoResult(st, hist, True)
-        if c >= LM_WINDOW:
+        if c - changed >= LM_WINDOW:
             prev = hist[c - LM_WINDOW][1]
             factor = (r.inf() / prev) ** (1.0 / LM_WINDOW) if prev > 0 else 0.0
+            new = sigma
             if factor > stall:
-                sigma = pb.K if sigma == 0 else 2.0 * sigma
+                new = pb.K if sigma == 0 else min(2.0 * sigma, LM_MAX_SHIFT * pb.K)
             elif sigma > 0:
-                sigma *= 0.5
-                if sigma < LM_MIN_SHIFT * pb.K:
-                    sigma = 0.0
+                new = 0.5 * sigma
+                if new < LM_MIN_SHIFT * pb.K:
+                    new = 0.0
+            if new != sigma:
+                sigma, changed = new, c
     return NsoResult(st, hist, False)

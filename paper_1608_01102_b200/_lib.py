@@ -66,6 +66,7 @@ SIGNATURES = {
     "smk_last_error": (ctypes.c_char_p, []),
     "smk_version": (I, []),
     "smk_launch_count": (ctypes.c_longlong, []),
+    "smk_pool_trim": (None, []),
     "smk_div": (I, [G, I, P, P, P]),
     "smk_grad": (I, [G, I, P, P, P]),
     "smk_zero_walls": (I, [G, I, P, P]),
@@ -98,6 +99,7 @@ SIGNATURES = {
                                        ctypes.POINTER(ctypes.c_longlong)]),
     "smk_nso_device_bytes": (I64, [P]),
     "smk_nso_set_guide": (I, [P, P, P, P]),
+    "smk_nso_set_K": (I, [P, D]),
     "smk_nso_vcycle": (I, [P, PS, P]),
     "smk_nso_residual_norms": (I, [P, PS, PD, PD, P]),
     "smk_nso_gauge_fix": (I, [P, PS, P]),

@@ -28,6 +28,8 @@ struct Scratch {
   ~Scratch();
 };
 
+// free the process-wide operator scratch pool (every device)
+void pool_trim();
 Geo coarsen(const Geo& g);
 Geo refine(const Geo& g);
 bool can_coarsen(const Geo& g);

@@ -811,31 +811,80 @@ using namespace smk;
 namespace smk {
 
 namespace {
+// Process-wide stream-ordered scratch pool: buffers return with an event
+// recorded on the releasing stream and are reused by size on the SAME device
+// (entries are keyed by (device, rounded size)); at most kPoolCap bytes stay
+// pooled per device, and smk_pool_trim() / an allocation failure hands them
+// back to the driver.
 struct PoolEntry {
   void* p;
   cudaStream_t st;
   cudaEvent_t ev;
 };
+using PoolKey = std::pair<int, size_t>;
 std::mutex g_pool_mu;
-std::multimap<size_t, PoolEntry> g_pool;   // rounded size -> free buffers
-constexpr size_t kPoolMax = size_t(1) << 30;
+std::multimap<PoolKey, PoolEntry> g_pool;
+std::map<int, size_t> g_pool_bytes;        // pooled bytes per device
+constexpr size_t kPoolMax = size_t(1) << 30;   // largest pooled buffer
+constexpr size_t kPoolCap = size_t(4) << 30;   // pooled bytes per device
 
 size_t pool_round(size_t b) {
   b = b < 256 ? 256 : b;
   return (b + 4095) & ~size_t(4095);
 }
+int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d;
+}
+// free every pooled buffer of device dev (-1: all devices)
+void pool_drop(int dev) {
+  std::vector<std::pair<PoolKey, PoolEntry>> drop;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (auto it = g_pool.begin(); it != g_pool.end();) {
+      if (dev < 0 || it->first.first == dev) {
+        drop.push_back(*it);
+        g_pool_bytes[it->first.first] -= it->first.second;
+        it = g_pool.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
+  const int here = cur_device();
+  for (auto& kv : drop) {
+    if (kv.first.first != here) cudaSetDevice(kv.first.first);
+    cudaEventSynchronize(kv.second.ev);
+    cudaEventDestroy(kv.second.ev);
+    cudaFree(kv.second.p);
+    if (kv.first.first != here) cudaSetDevice(here);
+  }
+}
 }  // namespace
+
+void pool_trim() { pool_drop(-1); }
 
 Scratch::~Scratch() { release(); }
 void Scratch::release() {
+  const int dev = cur_device();
   for (auto& b : bufs) {
     if (!b.first) continue;
     if (pooled && b.second <= kPoolMax) {
+      bool room;
+      {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        room = g_pool_bytes[dev] + b.second <= kPoolCap;
+      }
       cudaEvent_t ev = nullptr;
-      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+      if (room && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
           cudaEventRecord(ev, st) == cudaSuccess) {
         std::lock_guard<std::mutex> lk(g_pool_mu);
-        g_pool.emplace(b.second, PoolEntry{b.first, st, ev});
+        g_pool.emplace(PoolKey{dev, b.second}, PoolEntry{b.first, st, ev});
+        g_pool_bytes[dev] += b.second;
         continue;
       }
       cudaGetLastError();
@@ -848,14 +897,16 @@ void Scratch::release() {
 }
 void* Scratch::get(size_t bytes) {
   const size_t r = pool_round(bytes);
+  const int dev = cur_device();
   if (pooled && r <= kPoolMax) {
     PoolEntry e{nullptr, nullptr, nullptr};
     {
       std::lock_guard<std::mutex> lk(g_pool_mu);
-      auto it = g_pool.find(r);
+      auto it = g_pool.find(PoolKey{dev, r});
       if (it != g_pool.end()) {
         e = it->second;
         g_pool.erase(it);
+        g_pool_bytes[dev] -= r;
       }
     }
     if (e.p) {
@@ -868,17 +919,8 @@ void* Scratch::get(size_t bytes) {
   void* p = nullptr;
   if (cudaMalloc(&p, r) != cudaSuccess) {
     cudaGetLastError();
-    // out of memory: hand the pooled buffers back to the driver and retry
-    std::multimap<size_t, PoolEntry> drop;
-    {
-      std::lock_guard<std::mutex> lk(g_pool_mu);
-      drop.swap(g_pool);
-    }
-    for (auto& kv : drop) {
-      cudaEventSynchronize(kv.second.ev);
-      cudaEventDestroy(kv.second.ev);
-      cudaFree(kv.second.p);
-    }
+    // out of memory: hand this device's pooled buffers back and retry
+    pool_drop(dev);
     if (cudaMalloc(&p, r) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
@@ -1142,10 +1184,12 @@ static std::vector<double> host_pinv_laplacian(const Geo& g) {
 }
 
 struct PinvKey {
+  int dev;
   int dim, n0, n1, n2, per, dtype;
   long long hbits;
   bool operator<(const PinvKey& o) const {
-    return std::tie(dim, n0, n1, n2, per, dtype, hbits) < std::tie(o.dim, o.n0, o.n1, o.n2, o.per, o.dtype, o.hbits);
+    return std::tie(dev, dim, n0, n1, n2, per, dtype, hbits) <
+           std::tie(o.dev, o.dim, o.n0, o.n1, o.n2, o.per, o.dtype, o.hbits);
   }
 };
 static std::mutex g_pinv_mu;
@@ -1154,7 +1198,7 @@ static std::map<PinvKey, void*> g_pinv;
 const void* device_pinv(const Geo& g, int dtype) {
   long long hb;
   memcpy(&hb, &g.h, 8);
-  PinvKey key{g.dim, g.n[0], g.n[1], g.n[2], g.periodic, dtype, hb};
+  PinvKey key{cur_device(), g.dim, g.n[0], g.n[1], g.n[2], g.periodic, dtype, hb};
   std::lock_guard<std::mutex> lk(g_pinv_mu);
   auto it = g_pinv.find(key);
   if (it != g_pinv.end()) return it->second;
@@ -1479,6 +1523,7 @@ extern "C" {
 
 const char* smk_last_error(void) { return smk::g_err; }
 int smk_version(void) { return 1; }
+void smk_pool_trim(void) { smk::pool_trim(); }
 long long smk_launch_count(void) { return smk::g_launches.load(); }
 
 #define ST(s) ((cudaStream_t)(s))

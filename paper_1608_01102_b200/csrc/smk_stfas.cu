@@ -1381,6 +1381,7 @@ struct NsoBase {
   virtual int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) = 0;
   virtual int gauge(const smk_state* s, cudaStream_t st) = 0;
   virtual int levels() const = 0;
+  virtual int set_K(double K) = 0;
   virtual int ncolors() const = 0;
   virtual int level_residual(int l, const smk_state* s, const void* const vprev[], const void* const unext[],
                              const void* const vs[], const smk_residual* rhs, const smk_residual* out,
@@ -1520,6 +1521,15 @@ struct Nso : NsoBase {
   }
 
   int levels() const override { return (int)lv.size(); }
+  int set_K(double K) override {
+    if (!(K >= 0)) { set_error("K must be >= 0"); return SMK_ERR_ARG; }
+    if (K != prm.K) {
+      prm.K = K;
+      if (vc_exec) cudaGraphExecDestroy(vc_exec);   // the kernels take K/r by value
+      vc_exec = nullptr;
+    }
+    return SMK_OK;
+  }
   int profile(int enable) override {
     prof = enable != 0;
     for (int k = 0; k < NKIND; ++k) ev_used[k] = 0;
@@ -2076,6 +2086,12 @@ static NsoBase* make_nso(const smk_grid* g, const smk_nso_params* p) {
     using T = decltype(tag);
     auto* n = new Nso<T::DIM, T::PER, typename T::R>(to_geo(g), *p);
     if (!n->ok) {
+      // the operator scratch pool may hold the memory: release it, retry once
+      delete n;
+      pool_trim();
+      n = new Nso<T::DIM, T::PER, typename T::R>(to_geo(g), *p);
+    }
+    if (!n->ok) {
       delete n;
       set_error("nso: device allocation failed");
       return SMK_ERR_CUDA;
@@ -2151,6 +2167,13 @@ int64_t smk_nso_device_bytes(const smk_nso* h) { return h ? h->impl->bytes() : 0
 int smk_nso_set_guide(smk_nso* h, const void* const v0[], const void* const vstar[], void* stream) {
   if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
   return h->impl->set_guide(v0, vstar, (cudaStream_t)stream);
+}
+
+int smk_nso_set_K(smk_nso* h, double K) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  int rc = h->impl->set_K(K);
+  if (rc == SMK_OK) h->prm.K = K;
+  return rc;
 }
 
 int smk_nso_vcycle(smk_nso* h, const smk_state* s, void* stream) {

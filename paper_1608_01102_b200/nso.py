@@ -272,6 +272,10 @@ class StfasHierarchy:
         self._guide = (v0, vs)   # keep alive: the handle stores the pointers
         _lib.check(self._L.smk_nso_set_guide(self._h, _lib.ptrs(v0), _lib.ptrs(vs), _dev.stream()), "set_guide")
 
+    def set_K(self, K):
+        """Update K on the handle in place (the LM shift)."""
+        _lib.check(self._L.smk_nso_set_K(self._h, float(K)), "set_K")
+
     def vcycle(self, s):
         st = s.c_struct()
         _lib.check(self._L.smk_nso_vcycle(self._h, ctypes.byref(st), _dev.stream()), "vcycle")
@@ -339,20 +343,24 @@ def solve_nso(spec, cfg, v0, vstar, s=None, eps=1e-5, cycle_budget=50, relative=
 LM_WINDOW = 3          # cycles over which the reduction factor is measured
 LM_STALL = 0.95        # per-cycle factor above which the shift is raised
 LM_MIN_SHIFT = 1e-3    # shift (relative to K) below which it is dropped
+LM_MAX_SHIFT = 1e3     # cap on the shift (relative to K)
 
 
 def _solve_lm(spec, cfg, hier, v0, vstar, s, eps, relative, budget, stall=LM_STALL):
     """SPEC.md:347 LM safeguard, frozen as a proximal shift.
 
-    While the per-cycle reduction factor of ||f||_inf over the last
-    LM_WINDOW cycles exceeds LM_STALL, the K/r blocks get a shift sigma
-    (sigma = K, then doubled while stalled, halved while progressing, dropped
-    below LM_MIN_SHIFT K).  A shifted V-cycle solves the damped problem
-    K' = K + sigma with guide (K v* + sigma v^k) / K' (v^k = the iterate
-    entering the cycle): the K-term becomes K/r (v - v*) + sigma/r (v - v^k),
-    so every fixed point of the damped cycles is the undamped solution.  The
-    stop test always uses the undamped residual.  Raises NonConvergence when
-    the budget is exhausted."""
+    The per-cycle reduction factor of ||f||_inf over the last LM_WINDOW
+    cycles is tested once LM_WINDOW cycles have run since the last change of
+    the shift sigma: above LM_STALL sigma is raised (K, then doubled, capped
+    at LM_MAX_SHIFT K), otherwise halved and dropped below LM_MIN_SHIFT K.  A
+    shifted V-cycle solves the damped problem K' = K + sigma with guide
+    (K v* + sigma v^k) / K' (v^k = the iterate entering the cycle): the K-term
+    becomes K/r (v - v*) + sigma/r (v - v^k), so every fixed point of the
+    damped cycles is the undamped solution.  One damped hierarchy serves every
+    sigma (K updated in place, smk_nso_set_K) and its guide lives in
+    persistent buffers updated in place, so the captured V-cycle graph is
+    re-instantiated only when sigma changes.  The stop test always uses the
+    undamped residual.  Raises NonConvergence when the budget is exhausted."""
     dt = s.dtype
     v0d, vs = _guide(spec, v0, vstar, dt)
     ri, r2 = hier.residual_norms(s)
@@ -360,27 +368,25 @@ def _solve_lm(spec, cfg, hier, v0, vstar, s, eps, relative, budget, stall=LM_STA
     tol = eps * ri if relative else eps
     if ri <= tol:
         return hist
-    sigma = 0.0
-    damped = {}
+    sigma, changed = 0.0, 0
+    damped, guide = None, None
     N = s.N
     try:
         for c in range(1, budget + 1):
             if sigma > 0:
-                key = sigma
-                if key not in damped:
-                    dcfg = StfasConfig(**{**cfg.__dict__, "K": cfg.K + sigma})
-                    damped[key] = StfasHierarchy(spec, dcfg, N, dt)
-                hd = damped[key]
+                if damped is None:
+                    damped = StfasHierarchy(spec, cfg, N, dt)
+                    guide = tuple(g.clone() for g in vs)
+                    damped.set_guide(v0d, guide)
+                damped.set_K(cfg.K + sigma)
                 a, b = cfg.K / (cfg.K + sigma), sigma / (cfg.K + sigma)
-                guide = []
                 for k in range(spec.dim):
-                    g = vs[k].clone()
                     if N > 1:
-                        _axpby_dev(g[1:], s.V[k][:N - 1], b, a)
-                    guide.append(g)
-                hd.set_guide(v0d, tuple(guide))
-                hd.vcycle(s)
-                hd.gauge_fix(s)
+                        guide[k][1:].copy_(vs[k][1:])
+                        _axpby_dev(guide[k][1:], s.V[k][:N - 1], b, a)
+                damped.set_guide(v0d, guide)   # re-restricts the coarse guides
+                damped.vcycle(s)
+                damped.gauge_fix(s)
             else:
                 hier.vcycle(s)
                 hier.gauge_fix(s)
@@ -388,18 +394,21 @@ def _solve_lm(spec, cfg, hier, v0, vstar, s, eps, relative, budget, stall=LM_STA
             hist.append((c, ri, r2))
             if ri <= tol:
                 return hist
-            if c >= LM_WINDOW:
+            if c - changed >= LM_WINDOW:
                 prev = hist[c - LM_WINDOW][1]
                 factor = (ri / prev) ** (1.0 / LM_WINDOW) if prev > 0 else 0.0
+                new = sigma
                 if factor > stall:
-                    sigma = cfg.K if sigma == 0 else 2.0 * sigma
+                    new = cfg.K if sigma == 0 else min(2.0 * sigma, LM_MAX_SHIFT * cfg.K)
                 elif sigma > 0:
-                    sigma = 0.5 * sigma
-                    if sigma < LM_MIN_SHIFT * cfg.K:
-                        sigma = 0.0
+                    new = 0.5 * sigma
+                    if new < LM_MIN_SHIFT * cfg.K:
+                        new = 0.0
+                if new != sigma:
+                    sigma, changed = new, c
     finally:
-        for h in damped.values():
-            h.close()
+        if damped is not None:
+            damped.close()
     raise NonConvergence(f"STFAS (LM) cycle budget exhausted (residual {hist[-1][1]:.3e} > {tol:.3e})",
                          residual=hist[-1][1], context=f"{budget} V-cycles")
 

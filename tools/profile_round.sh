@@ -7,9 +7,9 @@
 set -e
 TAG=${1:-r01}
 CFG=${2:-5}
-CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu --no-e2e"
+CMD="python bench.py --config $CFG --steps 1 --warmup 1 --no-cpu --no-e2e --no-tts"
 mkdir -p gpurun_out
-python bench.py --config $CFG --steps 3 --warmup 3 > gpurun_out/${TAG}_c${CFG}_bench.json 2> gpurun_out/${TAG}_c${CFG}_bench.err
+python bench.py --config $CFG --steps 3 --warmup 3 --no-cpu > gpurun_out/${TAG}_c${CFG}_bench.json 2> gpurun_out/${TAG}_c${CFG}_bench.err
 $CMD > gpurun_out/${TAG}_c${CFG}_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --profile-from-start off -c 2000 --csv --log-file gpurun_out/${TAG}_c${CFG}_launches.csv $CMD \
