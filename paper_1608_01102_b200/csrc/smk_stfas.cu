@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstring>
 #include <vector>
+#include <array>
+#include <type_traits>
 
 #include "smk_internal.cuh"
 
@@ -1018,10 +1020,17 @@ struct BackIn {
   R VC[DIM][NB];
 };
 
-template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP>
+// FUSE (red-black, where every face of the grid has exactly one cell of the
+// colour): no delta buffer and no apply pass -- U, P and PBAR take
+// x += omega dx in place (no thread of the pass reads them), and V, which the
+// pass's stencils read, is written whole into the other buffer of a pair
+// (so.V = the pass's output, cx.V its input): Vout = Vin + omega dv at every
+// face.  Same arithmetic as k_scgs_apply, so bitwise equal to the unfused
+// pass.
+template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP, bool FUSE>
 __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
-                                                   R* __restrict__ xout) {
+                                                   R* __restrict__ xout, StP<R> so) {
   using LN = Line<DIM>;
   constexpr int NF = LN::NF, B = LN::B, NTT = CMP ? LN::NT : LN::NL;
   const auto& ix = cx.ix;
@@ -1079,10 +1088,30 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       ga += cg.gcol[q] * a[q];
     }
     const R dp = (ga - yu[NF]) * lc.isig;
-    R* xo = xout + (int64_t)(2 * ip) * B * M + m;
+    if constexpr (FUSE) {
+      R ou[NF];
 #pragma unroll
-    for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
-    xo[(int64_t)NF * M] = omega * dp;
+      for (int q = 0; q < NF; ++q)
+        if (!cg.wall[q]) ou[q] = so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]];
+      const int64_t oc = (int64_t)ip * cx.nc + L.co;
+      const R op = so.P[oc];
+#pragma unroll
+      for (int q = 0; q < NF; ++q)
+        if (!cg.wall[q]) so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = ou[q] + omega * (cg.gcol[q] * dp - a[q]);
+      so.P[oc] = op + omega * dp;
+    } else {
+      R* xo = xout + (int64_t)(2 * ip) * B * M + m;
+#pragma unroll
+      for (int q = 0; q < NF; ++q) xo[(int64_t)q * M] = cg.wall[q] ? R(0) : omega * (cg.gcol[q] * dp - a[q]);
+      xo[(int64_t)NF * M] = omega * dp;
+    }
+  };
+  // FUSE: V of frame ip (pair ip) = its input value (own faces of the frame's
+  // stencil) + omega dv
+  auto v_store = [&](int ip, const BackIn<DIM, R, CMP>& in, const R (&dv)[NF]) {
+#pragma unroll
+    for (int q = 0; q < NF; ++q)
+      if (!cg.wall[q]) so.V[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = in.VC[q >> 1][(q & 1) + 1] + omega * dv[q];
   };
   R xn[NF];   // dv of pair i+1
   R t[NF];    // M_{i+1} dv_{i+1}
@@ -1098,6 +1127,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       fetch(i, cur);
     }
     if (i + 1 < N) mdot(cur, xn, t);
+    if (FUSE && i + 1 < N) v_store(i + 1, cur, xn);
     if (i < 0) {
       R zero[NF];
 #pragma unroll
@@ -1144,9 +1174,14 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
 #pragma unroll
       for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
-    R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
+    if constexpr (FUSE) {
+      const int64_t oc = (int64_t)i * cx.nc + L.co;
+      so.PB[oc] = so.PB[oc] + omega * xb[NF];
+    } else {
+      R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
-    for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
+      for (int r = 0; r < B; ++r) xo[(int64_t)r * M] = omega * xb[r];
+    }
     if (i + 1 < N) {
       R dvi[NF];
 #pragma unroll
@@ -1513,6 +1548,11 @@ struct Nso : NsoBase {
     const int64_t per_pair = std::max((int64_t)Line<DIM>::SE * maxM, (int64_t)Line<DIM>::RS * rec_m);
     scratch = alloc((int64_t)N * per_pair);
     xout = alloc((int64_t)2 * N * B * maxM);
+    vswap.resize(lv.size());
+    for (size_t l = 0; l < lv.size(); ++l) {
+      for (int k = 0; k < 3; ++k)
+        vswap[l][k] = (k < DIM && fusable((int)l)) ? alloc((int64_t)N * lv[l].nf[k]) : nullptr;
+    }
     flag = (int*)mem.get(64);
     parts = (double*)mem.get(sizeof(double) * 70000);
     scal = mem.get(64);
@@ -1661,7 +1701,26 @@ struct Nso : NsoBase {
   }
   int kernel_mod() const { return prm.red_black ? -1 : prm.color_mod; }
 
+  // red-black passes whose backward is k_scgs_back run fused (no delta
+  // buffer, no apply kernel, V ping-pongs through vswap[l]); the record
+  // backward of the small colours keeps deltas + apply.  SMK_NO_FUSE=1 off.
+  bool fuse_env = getenv("SMK_NO_FUSE") == nullptr || atoi(getenv("SMK_NO_FUSE")) == 0;
+  bool fusable(int l) const {
+    if (!prm.red_black || !fuse_env) return false;
+    int o[3], mm[3];
+    const int64_t M = color_geometry(lv[l].g, 0, o, mm);
+    return !(M < fwd_mid && back_deep);
+  }
+  std::vector<std::array<R*, 3>> vswap;   // per level: the other V buffer of a fused pass pair
+
   void sweep(int l, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
+    if (fusable(l) && n_colors() == 2) {
+      StP<R> alt = s;
+      for (int k = 0; k < 3; ++k) alt.V[k] = vswap[l][k];
+      color_pass(l, 0, s, rhs, st, &alt);   // V: s -> alt
+      color_pass(l, 1, alt, rhs, st, &s);   // V: alt -> s
+      return;
+    }
     for (int col = 0; col < n_colors(); ++col) color_pass(l, col, s, rhs, st);
   }
 
@@ -1703,7 +1762,8 @@ struct Nso : NsoBase {
     else launch_fwd_t<TM, P, false, NX, FMT>(c, r, o, mod, mm, M, st);
   }
 
-  void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st) {
+  void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st,
+                  const StP<R>* fuse_out = nullptr) {
     const Level<R>& L = lv[l];
     const int mod = kernel_mod();
     auto c = ctx(l, s);
@@ -1737,15 +1797,29 @@ struct Nso : NsoBase {
     }
     prof_end(0, st);
     prof_begin(3, l, M, st);
+    StP<R> so{};
+    if (fuse_out) {
+      so = s;
+      for (int k = 0; k < 3; ++k) so.V[k] = fuse_out->V[k];
+    }
     {
       const int tpb = M >= 148 * 128 ? 128 : 32;
       const unsigned gb = (unsigned)((M + tpb - 1) / tpb);
+      auto back = [&](auto pipe, auto nxc, auto cmpc) {
+        constexpr bool PIPEv = decltype(pipe)::value, CMPv = decltype(cmpc)::value;
+        constexpr int NXv = decltype(nxc)::value;
+        if (fuse_out)
+          k_scgs_back<DIM, PER, R, PIPEv, NXv, CMPv, true><<<gb, tpb, 0, st>>>(
+              c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout, so);
+        else
+          k_scgs_back<DIM, PER, R, PIPEv, NXv, CMPv, false><<<gb, tpb, 0, st>>>(
+              c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout, so);
+      };
+      using F = std::false_type;
+      using T = std::true_type;
+      using Z = std::integral_constant<int, 0>;
       if (cmp) {
-        with_nx(l, [&](auto nxc) {
-          constexpr int NXv = decltype(nxc)::value;
-          k_scgs_back<DIM, PER, R, false, NXv, true><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
-                                                                        mm[2], (R)prm.omega, scratch, xout);
-        });
+        with_nx(l, [&](auto nxc) { back(F{}, nxc, T{}); });
       } else if (shape == 2 && back_deep) {   // record hand-off
         const size_t shm = (size_t)back_depth<R>() * 32 * rec_pitch<R>(Line<DIM>::RS) * sizeof(R);
         static bool attr = false;
@@ -1756,15 +1830,14 @@ struct Nso : NsoBase {
         k_scgs_back_deep<DIM, PER, R><<<(unsigned)((M + 31) / 32), 32, shm, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1],
                                                                                   mm[2], (R)prm.omega, scratch, xout);
       } else if (M >= back_flat) {
-        k_scgs_back<DIM, PER, R, false, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                                     (R)prm.omega, scratch, xout);
+        back(F{}, Z{}, F{});
       } else {
-        k_scgs_back<DIM, PER, R, true, 0, false><<<gb, tpb, 0, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2],
-                                                                    (R)prm.omega, scratch, xout);
+        back(T{}, Z{}, F{});
       }
       count_launch();
     }
     prof_end(3, st);
+    if (fuse_out) return;
     prof_begin(1, l, M, st);
     k_scgs_apply<DIM, PER, R, 1><<<frame_grid(M, prm.n_frames, 256), 256, 0, st>>>(
         ix, s, prm.n_frames, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], xout);
