@@ -63,6 +63,7 @@ class ControlResult:
     logs: list = field(default_factory=list)
     converged: bool = False
     vcycle_log: list = field(default_factory=list)   # (admm_iter, vcycle_index, residual_inf, residual_l2, wall_ms)
+    best_outer_iter: int = None     # MaxIterations: the iteration these fields come from
 
     def write_log_csv(self, path):
         """Per-iteration CSV: outer_iter, ao_obj, nso_resid, visual_diff, wall_s."""
@@ -104,6 +105,9 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
     Raises MaxIterations (``.result`` = best-so-far ControlResult) when
     max_outer iterations pass without the stop test; inner failures propagate
     annotated with the outer iteration."""
+    if dtype == torch.float32 and cfg.projection_tol < 1e-5:
+        raise ValueError(f"ADMM in float32 needs projection_tol >= 1e-5 (got {cfg.projection_tol:g}): the AO "
+                         "step's absolute projection tolerance is below the fp32 floor; run in float64")
     _dev.require_device()
     if not isinstance(keyframes, KeyframeSet):
         raise SmokeCtrlError("keyframes must be a KeyframeSet")
@@ -129,8 +133,9 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
     hier = StfasHierarchy(spec, ncfg, n, dtype)
     logs = []
     vlog = []
-    result = None
+    best = None
     prev_aug = None
+    suspended = bool(cfg.fallback)   # fallback: lambda frozen until the augmented objective stalls
     t_start = time.perf_counter()
     try:
         for it in range(1, cfg.max_outer + 1):
@@ -160,23 +165,37 @@ def run(spec, rho0, keyframes, cfg, metric=None, v0=None, dtype=torch.float64):
             diff = inf_norm(_axpby(rho_last.clone(), rho, 1.0, -1.0))
             logs.append({"outer_iter": it, "ao_obj": ao_obj, "nso_resid": hist[-1][1], "visual_diff": diff,
                          "wall_s": time.perf_counter() - t_start})
-            result = ControlResult(rho=rho, v=tuple(c.clone() for c in v), u=tuple(s.U), vstar=vstar,
-                                   lam=tuple(c.clone() for c in lam), state=s, logs=logs, vcycle_log=vlog)
             if diff < eps_admm:
-                result.converged = True
-                return result
+                return ControlResult(rho=rho, v=tuple(c.clone() for c in v), u=tuple(s.U), vstar=vstar,
+                                     lam=tuple(c.clone() for c in lam), state=s, logs=logs, converged=True,
+                                     vcycle_log=vlog)
+            # best so far: the smallest visual difference; its
+            # fields are copied (the live state keeps iterating)
+            if best is None or diff < best.logs[-1]["visual_diff"]:
+                sb = s.copy()
+                best = ControlResult(rho=rho, v=tuple(c.clone() for c in v), u=tuple(sb.U), vstar=vstar,
+                                     lam=tuple(c.clone() for c in lam), state=sb, logs=list(logs),
+                                     vcycle_log=list(vlog))
             rho_last = rho
-            if cfg.fallback:
+            if suspended:
+                # the multiplier update is suspended once: from
+                # the first iteration while the augmented objective still drops
+                # by more than fallback_tol; the first iteration that does not
+                # ends the suspension for good
                 aug = _augmented(spec, cfg, rho, keyframes, s, v, vstar, lam)
                 dropping = prev_aug is not None and aug < prev_aug * (1.0 - cfg.fallback_tol)
+                first = prev_aug is None
                 prev_aug = aug
-                if dropping or it == 1:
+                if first or dropping:
                     continue
+                suspended = False
             for lc, vc, sc in zip(lam, v, vstar):
                 d = _axpby(vc.clone(), sc, -1.0, 1.0)
                 _axpby(lc, d, cfg.K * cfg.beta, 1.0)
-            result.lam = tuple(c.clone() for c in lam)
-        raise MaxIterations(f"ADMM did not reach eps_ADMM={eps_admm:g} in {cfg.max_outer} outer iterations",
-                            result=result)
+        b_it, b_diff = best.logs[-1]["outer_iter"], best.logs[-1]["visual_diff"]
+        best.best_outer_iter = b_it
+        best.logs, best.vcycle_log = logs, vlog     # the full history rides along
+        raise MaxIterations(f"ADMM did not reach eps_ADMM={eps_admm:g} in {cfg.max_outer} outer iterations "
+                            f"(best visual difference {b_diff:.3e} at outer iteration {b_it})", result=best)
     finally:
         hier.close()

@@ -1,7 +1,11 @@
 """Seeded synthetic workloads of BASELINE.json (configs 1-5).
 
 The paper's keyframe assets are not available; these seeded
-stand-ins keep the configs' shapes, sizes and value distributions.  The STFAS
+stand-ins keep the configs' shapes, sizes and value distributions: the
+initial densities and keyframes are the ones BASELINE.json's configs describe
+(``initial_density``, ``keyframes``; unspecified parameters per SURVEY.md
+§8d: threshold 0.5 of the max-normalised sum, then a Gaussian blur of sigma
+= 1 cell, clipped at 0 because KeyframeSet rejects negatives, ao.py:40-41).  The STFAS
 input v* is the throughput-mode guide of SURVEY.md §8d: a band-limited random
 face field (recipe of pkg/tests/oracles.py:46-66) projected solenoidal on the
 GPU and scaled so that dt*|v*|_inf/h = 1.  Generation runs on the device with
@@ -117,24 +121,91 @@ def _cell_centres(spec, device="cuda"):
     return torch.meshgrid(*ax, indexing="ij")
 
 
-def gaussian(spec, centre, sigma):
-    x = _cell_centres(spec)
+def gaussian(spec, centre, sigma, device="cuda"):
+    x = _cell_centres(spec, device)
     r2 = sum((xi - ci) ** 2 for xi, ci in zip(x, centre))
     return torch.exp(-r2 / (2 * sigma * sigma))
 
 
-def initial_density(w):
+def initial_density(w, device="cuda"):
     """BASELINE.json initial densities (seeded where the config says so)."""
     gen = np.random.default_rng(SEED_BASE + w.index)
     s = w.spec
     if w.index == 1:
-        return gaussian(s, (0.5, 0.25), 0.08)
+        return gaussian(s, (0.5, 0.25), 0.08, device)
     if w.index == 2:
-        return gaussian(s, (0.5, 0.2), 0.06)
+        return gaussian(s, (0.5, 0.2), 0.06, device)
     if w.index == 4:
-        return gaussian(s, (0.5, 0.2, 0.5), 0.08)
+        return gaussian(s, (0.5, 0.2, 0.5), 0.08, device)
     n_g = 4
     lo, hi = (0.03, 0.08) if w.dim == 2 else (0.04, 0.1)
     cen = gen.uniform(0.2, 0.8, size=(n_g, w.dim))
     sig = gen.uniform(lo, hi, size=n_g)
-    return sum(gaussian(s, tuple(c), float(sg)) for c, sg in zip(cen, sig))
+    return sum(gaussian(s, tuple(c), float(sg), device) for c, sg in zip(cen, sig))
+
+
+def _blur_axis(x, axis, sigma=1.0, truncate=4.0):
+    """1-D Gaussian blur (sigma in cells, reflect at the domain walls, taps to
+    truncate * sigma: scipy.ndimage.gaussian_filter's defaults)."""
+    r = int(truncate * sigma + 0.5)
+    t = torch.arange(-r, r + 1, dtype=torch.float64, device=x.device)
+    wts = torch.exp(-0.5 * (t / sigma) ** 2)
+    wts = wts / wts.sum()
+    n = x.shape[axis]
+    idx = torch.arange(-r, n + r, device=x.device)
+    idx = torch.where(idx < 0, -idx - 1, idx)            # reflect (d c b a | a b c d)
+    idx = torch.where(idx >= n, 2 * n - 1 - idx, idx)
+    xp = torch.index_select(x, axis, idx)
+    out = torch.zeros_like(x)
+    for k in range(2 * r + 1):
+        out += wts[k] * torch.narrow(xp, axis, k, n)
+    return out
+
+
+def blur(x, sigma=1.0):
+    for a in range(x.dim()):
+        x = _blur_axis(x, a, sigma)
+    return x
+
+
+def _threshold_smooth(field):
+    """Threshold at 0.5 of the max, then blur sigma = 1 cell."""
+    m = (field / field.max() >= 0.5).to(torch.float64)
+    return blur(m, 1.0).clamp_min(0.0)
+
+
+def _gauss_sum(spec, gen, count, lo, hi, device):
+    cen = gen.uniform(0.2, 0.8, size=(count, spec.dim))
+    sig = gen.uniform(lo, hi, size=count)
+    return sum(gaussian(spec, tuple(c), float(sg), device) for c, sg in zip(cen, sig))
+
+
+def keyframes(w, device="cuda"):
+    """BASELINE.json keyframes {timestep: density (fp64)}.
+
+    cfg1: disc r = 0.15 at (0.5, 0.7) with a smoothstep edge of +-1 cell at
+    t = 16; cfg2: the letter-F mask (three rectangles) blurred by sigma = 1
+    cell at t = 40; cfg3: t = 30, 60, each 6 seeded Gaussians (sigma
+    U[0.03, 0.08]) thresholded and smoothed; cfg4: t = 60, 8 seeded 3D
+    Gaussians (sigma U[0.04, 0.1]); cfg5: t = 20, 40, 60, 80, 8 seeded
+    Gaussians each.  The seeded draws continue initial_density's stream
+    (its centres and sigmas first, then each keyframe in time order)."""
+    s = w.spec
+    x = _cell_centres(s, device)
+    if w.index == 1:
+        d = torch.sqrt((x[0] - 0.5) ** 2 + (x[1] - 0.7) ** 2)
+        a, b = 0.15 - s.h, 0.15 + s.h
+        t = ((d - a) / (b - a)).clamp(0.0, 1.0)
+        return {16: 1.0 - t * t * (3.0 - 2.0 * t)}
+    if w.index == 2:
+        inside = lambda x0, x1, y0, y1: (x[0] >= x0) & (x[0] <= x1) & (x[1] >= y0) & (x[1] <= y1)
+        f = inside(0.35, 0.45, 0.3, 0.8) | inside(0.35, 0.7, 0.7, 0.8) | inside(0.35, 0.6, 0.5, 0.58)
+        return {40: blur(f.to(torch.float64), 1.0).clamp_min(0.0)}
+    gen = np.random.default_rng(SEED_BASE + w.index)
+    lo, hi = (0.03, 0.08) if w.dim == 2 else (0.04, 0.1)
+    if w.index != 4:                       # initial_density's draws come first
+        gen.uniform(0.2, 0.8, size=(4, w.dim))
+        gen.uniform(lo, hi, size=4)
+    times = {3: (30, 60), 4: (60,), 5: (20, 40, 60, 80)}[w.index]
+    count = {3: 6, 4: 8, 5: 8}[w.index]
+    return {t: _threshold_smooth(_gauss_sum(s, gen, count, lo, hi, device)) for t in times}

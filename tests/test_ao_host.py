@@ -34,3 +34,21 @@ def test_keyframe_and_metric_validation():
         GaussianMetric(spec, levels=0)
     with pytest.raises(ValueError):
         GaussianMetric(spec, levels=2, weights=(1.0,))
+
+
+def test_fp32_ao_needs_a_reachable_projection_tolerance():
+    """the reference's absolute projection_tol (1e-9) is below the
+    fp32 floor; fp32 AO / ADMM is rejected up front instead of exhausting the
+    Poisson budget on every frame."""
+    import torch
+    from paper_1608_01102_b200 import admm
+    from paper_1608_01102_b200.ao import AoConfig, GaussianMetric, KeyframeSet, solve_ao
+    from paper_1608_01102_b200.fields import GridSpec
+    spec = GridSpec(2, (8, 8), 1 / 8)
+    vg = tuple(torch.zeros((3,) + spec.face_shape(k), dtype=torch.float32) for k in range(2))
+    rho0 = torch.zeros((8, 8), dtype=torch.float32)
+    kf = KeyframeSet(3, {3: np.ones((8, 8))})
+    with pytest.raises(ValueError, match="float32"):
+        solve_ao(spec, vg, rho0, kf, None, AoConfig(K=1.0, dt=0.25))
+    with pytest.raises(ValueError, match="float32"):
+        admm.run(spec, rho0, kf, admm.AdmmConfig(dt=0.25), dtype=torch.float32)

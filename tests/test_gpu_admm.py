@@ -24,7 +24,7 @@ def _problem():
     return rho0, target
 
 
-def _both(eps_admm, max_outer, tmp_path=None):
+def _both(eps_admm, max_outer, tmp_path=None, fallback=False):
     from oracle import admm as oadmm
     from oracle.grid import Grid
     from paper_1608_01102_b200 import admm, ao, fields
@@ -32,21 +32,24 @@ def _both(eps_admm, max_outer, tmp_path=None):
     rho0, target = _problem()
     g = Grid(2, (8, 8), 0.125, "neumann")
     ref = oadmm.run(g, rho0, {N: target}, N, DT, K=K, r=R, eps_stfas=1e-9, eps_admm=eps_admm,
-                    max_outer=max_outer, nso_cycle_budget=100)
+                    max_outer=max_outer, nso_cycle_budget=100, fallback=fallback)
     spec = fields.GridSpec(2, (8, 8), 0.125, "neumann")
     cfg = admm.AdmmConfig(dt=DT, K=K, r=R, eps_stfas=1e-9, eps_admm=eps_admm, max_outer=max_outer,
-                          nso_cycle_budget=100)
+                          nso_cycle_budget=100, fallback=fallback)
     try:
         res = admm.run(spec, rho0, ao.KeyframeSet(N, {N: target}), cfg)
     except MaxIterations as e:
         res = e.result
         assert not ref["converged"]
+        # the exception carries the best-so-far iteration
+        assert res.best_outer_iter == ref["best"]["logs"][-1]["outer_iter"]
     return ref, res
 
 
 def _compare(ref, res):
     assert res.converged == ref["converged"]
     assert len(res.logs) == len(ref["logs"])
+    ref = ref if ref["converged"] else dict(ref["best"], logs=ref["logs"])
     for a, b in zip(res.logs, ref["logs"]):
         assert a["outer_iter"] == b["outer_iter"]
         assert abs(a["visual_diff"] - b["visual_diff"]) <= 1e-6 * b["visual_diff"]
@@ -83,3 +86,42 @@ def test_admm_max_iterations_with_multiplier_updates():
     ref, res = _both(1e-7, 3)
     assert not ref["converged"] and len(res.logs) == 3
     _compare(ref, res)
+
+
+def test_admm_fallback_suspends_multiplier_updates_once():
+    """fallback=True: lambda frozen from the first iteration
+    while the augmented objective drops, then updated for good; GPU and
+    oracle follow the same path."""
+    ref, res = _both(1e-7, 4, fallback=True)
+    assert not ref["converged"]
+    _compare(ref, res)
+
+
+def test_admm_cfg1_baseline_keyframe_matches_oracle():
+    """BASELINE cfg1 (2D 32^2 x 16, r = 1e-3, 2-level STFAS, disc keyframe
+    with a smoothstep edge at t = 16, Gaussian initial density): the whole
+    ADMM loop on the GPU vs oracle/admm.py with the C NSO (same algorithm,
+    tests/test_coracle.py) -- final rho, v, u, v* and the objective."""
+    import torch
+    from oracle import admm as oadmm
+    from oracle.grid import Grid
+    from paper_1608_01102_b200 import admm, ao, workloads
+    w = workloads.config(1)
+    rho0 = workloads.initial_density(w).cpu().numpy()
+    kf = {t: k.cpu().numpy() for t, k in workloads.keyframes(w).items()}
+    g = Grid(2, (32, 32), 1 / 32, "neumann")
+    ref = oadmm.run(g, rho0, kf, w.N, w.dt, K=w.K, r=w.r, eps_stfas=1e-5, max_outer=3, nso_cycle_budget=400,
+                    n_levels=w.levels, nso="c")
+    cfg = admm.AdmmConfig(dt=w.dt, K=w.K, r=w.r, eps_stfas=1e-5, max_outer=3, nso_cycle_budget=400,
+                          n_levels=w.levels)
+    res = admm.run(w.spec, rho0, ao.KeyframeSet(w.N, kf), cfg)
+    assert res.converged == ref["converged"] and len(res.logs) == len(ref["logs"])
+    t = lambda xs: tuple(x.cpu().numpy() for x in xs)
+    assert rel_err(res.rho.cpu().numpy(), ref["rho"]) < 1e-8
+    assert rel_err(t(res.vstar), ref["vstar"]) < 1e-8
+    assert rel_err(t(res.v), ref["v"]) < 1e-8
+    assert rel_err(t(res.u), ref["state"].U) < 1e-8
+    obj_g = admm.objective(res.rho, ao.KeyframeSet(w.N, kf), res.u, w.r)
+    obj_c = oadmm.objective(ref["rho"], kf, ref["state"].U, w.r)
+    print(f"[parity] cfg1 ADMM: {len(res.logs)} outer iterations, objective gpu {obj_g:.10e} oracle {obj_c:.10e}")
+    assert abs(obj_g - obj_c) <= 1e-8 * abs(obj_c)
