@@ -152,7 +152,9 @@ typedef struct smk_nso_params {
 } smk_nso_params;
 
 /* Spacetime state (pair index i = 0..N-1): V[i]=v_{i+1}, PB[i]=pbar_{i+1},
- * U[i]=u_i, P[i]=p_{i+1}; every array has N frames. */
+ * U[i]=u_i, P[i]=p_{i+1}; every array has N frames.  Neumann wall faces are
+ * not unknowns and must hold zero (zero_boundary_faces, fields.py:145-160);
+ * the solver never writes them. */
 typedef struct smk_state {
   void* V[3];
   void* PB;

@@ -1018,6 +1018,9 @@ struct BackIn {
   // compact: D~ faces block + rhs; factored: L + 1/d + z
   R t[CMP ? NF * (NF + 1) / 2 : B * (B - 1) / 2], b[B], d[CMP ? 1 : B], yu[B];
   R VC[DIM][NB];
+  // FUSE: the in-place targets of the step (U, P of pair i+1, PBAR of pair i),
+  // loaded with the step's other inputs so no extra latency joins the chain
+  R uo[NF], po, pbo;
 };
 
 // FUSE (red-black, where every face of the grid has exactly one cell of the
@@ -1064,6 +1067,15 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       for (int q = 0; q < B; ++q) in.yu[q] = sc(i + 1, LN::Y0 + q);
       load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i + 1, cx.nf), in.VC);
     }
+    if constexpr (FUSE) {
+      if (i + 1 < N) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+          in.uo[q] = cg.wall[q] ? R(0) : so.U[q >> 1][(int64_t)(i + 1) * cx.nf[q >> 1] + L.of[q]];
+        in.po = so.P[(int64_t)(i + 1) * cx.nc + L.co];
+      }
+      if (i >= 0) in.pbo = so.PB[(int64_t)i * cx.nc + L.co];
+    }
   };
   // t = M dv from a V stencil
   auto mdot = [&](const BackIn<DIM, R, CMP>& in, const R (&dv)[NF], R (&t)[NF]) {
@@ -1078,7 +1090,8 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
     }
   };
   // du, dp of pair ip from dv_ip (dvi), yu_ip and t = M_ip dv_{ip+1}
-  auto u_delta = [&](int ip, const R (&yu)[B], const R (&dvi)[NF], const R (&t)[NF]) {
+  auto u_delta = [&](int ip, const BackIn<DIM, R, CMP>& in, const R (&dvi)[NF], const R (&t)[NF]) {
+    const auto& yu = in.yu;
     R a[NF];
     R ga = R(0);
 #pragma unroll
@@ -1089,16 +1102,11 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
     }
     const R dp = (ga - yu[NF]) * lc.isig;
     if constexpr (FUSE) {
-      R ou[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q)
-        if (!cg.wall[q]) ou[q] = so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]];
-      const int64_t oc = (int64_t)ip * cx.nc + L.co;
-      const R op = so.P[oc];
-#pragma unroll
-      for (int q = 0; q < NF; ++q)
-        if (!cg.wall[q]) so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = ou[q] + omega * (cg.gcol[q] * dp - a[q]);
-      so.P[oc] = op + omega * dp;
+        if (!cg.wall[q])
+          so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = in.uo[q] + omega * (cg.gcol[q] * dp - a[q]);
+      so.P[(int64_t)ip * cx.nc + L.co] = in.po + omega * dp;
     } else {
       R* xo = xout + (int64_t)(2 * ip) * B * M + m;
 #pragma unroll
@@ -1132,7 +1140,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       R zero[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) zero[q] = R(0);
-      u_delta(0, cur.yu, zero, t);   // dv_0 = 0 (pinned / frozen halo)
+      u_delta(0, cur, zero, t);   // dv_0 = 0 (pinned / frozen halo)
       break;
     }
     R T[B][B], dinv[B], xb[B];
@@ -1175,8 +1183,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
     if constexpr (FUSE) {
-      const int64_t oc = (int64_t)i * cx.nc + L.co;
-      so.PB[oc] = so.PB[oc] + omega * xb[NF];
+      so.PB[(int64_t)i * cx.nc + L.co] = cur.pbo + omega * xb[NF];
     } else {
       R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
@@ -1186,7 +1193,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
       R dvi[NF];
 #pragma unroll
       for (int q = 0; q < NF; ++q) dvi[q] = xb[q];
-      u_delta(i + 1, cur.yu, dvi, t);
+      u_delta(i + 1, cur, dvi, t);
     }
 #pragma unroll
     for (int q = 0; q < NF; ++q) xn[q] = xb[q];

@@ -221,6 +221,14 @@ def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
     P = 0.1 * torch.randn((N, n, n, n), generator=g, dtype=torch.float64)
     vs = tuple((0.1 * torch.randn(shp(k), generator=g, dtype=torch.float64)) for k in range(3))
     v0 = tuple(torch.zeros(shp(k)[1:], dtype=torch.float64) for k in range(3))
+    # the state carries zero wall faces (zero_boundary_faces, fields.py:145-160)
+    for k in range(3):
+        for c in (V[k], U[k], vs[k]):
+            idx = [slice(None)] * 4
+            idx[k + 1] = 0
+            c[tuple(idx)] = 0
+            idx[k + 1] = -1
+            c[tuple(idx)] = 0
     outs = []
     for fwd, bf in [("tm64p1", 0), ("tm32p2", 1 << 40), ("tm32p4", 1 << 40)]:
         shape_env(fwd, bf)
