@@ -34,9 +34,14 @@ def build(force=False, verbose=True):
     os.makedirs(objdir, exist_ok=True)
     procs = []
     objs = []
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
+    hdr_t = max(hdr_t, os.path.getmtime(os.path.join(ROOT, "include", "smk.h")))
     for src in SOURCES:
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
         objs.append(obj)
+        # per-object incremental: rebuild only sources (or shared headers) newer than the object
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(os.path.join(CSRC, src))):
+            continue
         cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

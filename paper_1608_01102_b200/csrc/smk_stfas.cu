@@ -389,10 +389,31 @@ struct Slots {
 // cells with (sum_a c_a) % 2 == o0 -- unit stride on the leading axes, stride
 // 2 along the last axis starting at the row's parity (even last extent, so
 // every row holds m_last colour cells).
+//
+// 3D red-black row order (mod = -T, T > 1): consecutive rows (one CTA each
+// on the big colours) walk axis 1 inside bands of T rows along axis 0, row
+// r -> (c0, c1) = (T (r / (T n1)) + r mod T, (r mod (T n1)) / T).  CTAs start
+// in blockIdx order and march through the N pairs independently, so a row's
+// stencil neighbours come from L2 only if their CTAs run close in time: with
+// the plain order (T = 1) the axis-0 neighbours are n1 rows away (a fifth of
+// the resident CTAs at 128^3, ~17 pairs of skew) and every neighbour row was
+// re-read from DRAM; with T = 8 the axis-1 neighbours are T rows away, the
+// axis-0 ones inside the band 1 row, and only the band edges miss.  A pure
+// relabelling of m: the pass's results do not depend on it.
 template <int DIM>
 __device__ __forceinline__ void color_cell(int64_t m, int o0, int o1, int o2, int mod, int m1, int m2, int (&c)[3]) {
   int64_t q = m;
   const int q2 = (int)(q % m2); q /= m2;
+  if (DIM == 3 && mod < -1) {
+    const int T = -mod;   // the host only passes T > 1 when T divides n0
+    const int64_t bw = (int64_t)T * m1;
+    const int64_t band = q / bw;
+    const int rem = (int)(q - band * bw);
+    c[0] = (int)(band * T) + rem % T;
+    c[1] = rem / T;
+    c[2] = ((o0 + c[0] + c[1]) & 1) + 2 * q2;
+    return;
+  }
   const int q1 = (int)(q % m1); q /= m1;
   if (mod > 0) {
     c[0] = o0 + mod * (int)q;
@@ -1706,7 +1727,14 @@ struct Nso : NsoBase {
     }
     return (int64_t)mm[0] * mm[1] * mm[2];
   }
-  int kernel_mod() const { return prm.red_black ? -1 : prm.color_mod; }
+  // 3D red-black: -T selects the banded row order of color_cell (T rows
+  // along axis 0 per band, T | n0); SMK_ROW_TILE overrides T (1 = plain)
+  int row_tile = getenv("SMK_ROW_TILE") ? atoi(getenv("SMK_ROW_TILE")) : 8;
+  int kernel_mod(int l) const {
+    if (!prm.red_black) return prm.color_mod;
+    if (DIM == 3 && row_tile > 1 && lv[l].g.n[0] % row_tile == 0) return -row_tile;
+    return -1;
+  }
 
   // red-black passes whose backward is k_scgs_back run fused (no delta
   // buffer, no apply kernel, V ping-pongs through vswap[l]); the record
@@ -1772,7 +1800,7 @@ struct Nso : NsoBase {
   void color_pass(int l, int col, const StP<R>& s, const ResP<R>* rhs, cudaStream_t st,
                   const StP<R>* fuse_out = nullptr) {
     const Level<R>& L = lv[l];
-    const int mod = kernel_mod();
+    const int mod = kernel_mod(l);
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     Ix<DIM, PER> ix(L.g);

@@ -117,6 +117,21 @@ def main():
         put(tag, "step_v", s1.v.comps)
         put(tag, "step_p", s1.p.values)
         put(tag, "step_rho", s1.rho.values)
+        # scalar_stencil_v_adjoint (advection.py:105) and the AdvectionOperator
+        # methods (advection.py:213-248) on a velocity with nonzero wall faces
+        # (the operator masks them at construction)
+        put(tag, "svadj", A.scalar_stencil_v_adjoint(spec, rho, mu))
+        vr = tuple(0.3 * rng.standard_normal(spec.face_shape(k)) for k in range(dim))
+        put(tag, "vraw", vr)
+        op = A.AdvectionOperator(F.StaggeredVectorField(spec, vr))
+        put(tag, "aop_st", op.apply_stencil(F.ScalarField(spec, rho)).values)
+        a2, r2 = op.advect(F.ScalarField(spec, rho), 0.1)
+        put(tag, "aop_adv", a2.values)
+        put(tag, "aop_k", np.array(r2.k_used))
+        b2, _ = op.jacobian_rho_T(F.ScalarField(spec, mu), 0.1, k_fixed=r2.k_used)
+        put(tag, "aop_rT", b2.values)
+        put(tag, "aop_vT", op.jacobian_v_T(F.ScalarField(spec, rho), F.ScalarField(spec, mu), 0.1,
+                                           k_fixed=r2.k_used).comps)
 
     # AO sweep (2D, both boundaries): one sweep from guiding = v*
     for tag, bnd, seed in [("ao2p", "periodic", 7), ("ao2n", "neumann", 8)]:

@@ -141,3 +141,34 @@ def test_determinism(smk):
     a, _ = A.advect_scalar(s, v, rho, 0.02)
     b, _ = A.advect_scalar(s, v, rho, 0.02)
     assert np.array_equal(a, b)
+
+
+def test_scalar_stencil_v_adjoint(case, smk):
+    """``advection.scalar_stencil_v_adjoint`` (``advection.py:105``) through
+    ``smk_scalar_stencil_v_adjoint`` (k_stencil_v_adj) vs the reference."""
+    _, F, A, _ = smk
+    s = spec_of(case, F)
+    got = A.scalar_stencil_v_adjoint(s, case["rho"], case["mu"])
+    assert rel_err(got, case.comps("svadj")) < 1e-14
+
+
+def test_advection_operator(case, smk):
+    """``AdvectionOperator`` (``advection.py:213-248``) built from a velocity
+    with nonzero wall faces (masked at construction) vs the reference's own
+    operator on the same raw velocity."""
+    _, F, A, _ = smk
+    s = spec_of(case, F)
+    op = A.AdvectionOperator(F.StaggeredVectorField(s, case.comps("vraw")))
+    rho = F.ScalarField(s, case["rho"])
+    mu = F.ScalarField(s, case["mu"])
+    h = lambda t: t.detach().cpu().numpy()
+    assert rel_err(h(op.apply_stencil(rho).values), case["aop_st"]) < 1e-14
+    out, rep = op.advect(rho, 0.1)
+    assert rep.k_used == int(case["aop_k"])
+    assert rel_err(h(out.values), case["aop_adv"]) < 1e-13
+    back, _ = op.jacobian_rho_T(mu, 0.1, k_fixed=rep.k_used)
+    assert rel_err(h(back.values), case["aop_rT"]) < 1e-13
+    gv = tuple(h(c) for c in op.jacobian_v_T(rho, mu, 0.1, k_fixed=rep.k_used).comps)
+    assert rel_err(gv, case.comps("aop_vT")) < 1e-13
+    with pytest.raises(ValueError):
+        op.advect(rho, 0.0)

@@ -208,7 +208,13 @@ def test_fp32_sweep_every_kernel_shape(nso, shape_env, fwd):
 
 def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
     """3D 64^3 x 6 fp64 (32^3 cells per colour -- the bench's fine-level
-    regime): one sweep with every shape; all agree to rounding."""
+    regime): one sweep with every forward shape vs the C oracle
+    (oracle/cstfas.c) on the same state, <= 1e-10 (the colour-pass bound);
+    the shapes order their fp64 algebra differently (prep mode, factored vs
+    compact hand-off), so they agree with each other to ~1e-11, not bitwise."""
+    import numpy as np
+    from oracle import cstfas, stfas
+    from oracle.grid import Grid
     from paper_1608_01102_b200.fields import GridSpec
     n, N = 64, 6
     spec = GridSpec(3, (n, n, n), 1.0 / n, "neumann")
@@ -236,13 +242,19 @@ def test_shapes_agree_on_bench_sized_colours(nso, shape_env):
                                              P.numpy(), dtype=torch.float64)
         nso.scgs_smooth(spec, cfg, dev, [c.numpy() for c in v0], [c.numpy() for c in vs])
         outs.append(dev.numpy())
-    for o in outs[1:]:
-        for a, b in zip(outs[0], o):
+    cstfas.load()
+    og = Grid(3, (n, n, n), 1.0 / n, "neumann")
+    pb = stfas.Problem(og, 1.0 / N, 1e3, 1e3, tuple(c.numpy() for c in v0), tuple(c.numpy() for c in vs))
+    st = stfas.State(tuple(c.numpy() for c in V), PB.numpy(), tuple(c.numpy() for c in U), P.numpy())
+    want = cstfas.scgs_smooth(pb, st)
+    wl = (want.V, want.PB, want.U, want.P)
+    for o in outs:
+        for a, b in zip(o, wl):
             if isinstance(a, (tuple, list)):
                 for x, y in zip(a, b):
-                    assert rel_err(x, y) < 1e-12
+                    assert rel_err(x, y) < 1e-10
             else:
-                assert rel_err(a, b) < 1e-12
+                assert rel_err(a, np.asarray(b)) < 1e-10
 
 
 @pytest.mark.parametrize("n", [64, 128])

@@ -118,3 +118,19 @@ def test_metric_3d_periodic(golden):
     metric = sim.GaussianMetric(g, levels=2, weights=(1.0, 0.5))
     assert rel_err(metric.apply(c["x"]), c["apply"]) < 1e-13
     assert abs(metric.quad(c["x"]) - float(c["quad"])) <= 1e-13 * float(c["quad"])
+
+
+def test_scalar_stencil_v_adjoint_and_operator_masking(case):
+    """``advection.py:105-130`` and the AdvectionOperator's wall masking
+    (``advection.py:220-224``): the oracle on the masked velocity equals the
+    reference operator built from the raw one."""
+    g = case.grid()
+    rho, mu = case["rho"], case["mu"]
+    assert rel_err(ops.scalar_stencil_v_adjoint(g, rho, mu), case.comps("svadj")) < 1e-14
+    vm = ops.zero_walls(g, case.comps("vraw"))
+    assert rel_err(ops.transport_scalar(g, vm, rho), case["aop_st"]) < 1e-14
+    out, k, _ = ops.taylor(g, vm, rho, 0.1)
+    assert k == int(case["aop_k"])
+    assert rel_err(out, case["aop_adv"]) < 1e-13
+    assert rel_err(ops.taylor(g, vm, mu, 0.1, k_fixed=k, transpose=True)[0], case["aop_rT"]) < 1e-13
+    assert rel_err(ops.advect_v_T(g, vm, rho, mu, 0.1, k), case.comps("aop_vT")) < 1e-13
