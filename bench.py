@@ -11,9 +11,10 @@ resident in HBM.  Default workload: BASELINE config 5 (3D 128^3 x 80 fp32,
     python bench.py --impl reference ...   # CPU oracle (port) on host cores
 
 Multi-GPU (N>1, torchrun): the spacetime volume is split into N contiguous
-time slabs, one per rank (strong scaling: total work fixed); halos go over
-NCCL (torch.distributed P2P) before every residual / colour pass and ||f|| is
-an allreduce(max) -- paper_1608_01102_b200/slabs.py, DESIGN.md §6.
+time slabs, one per rank (strong scaling: total work fixed), on libsmk's C++
+slab set: the whole V-cycle is one CUDA graph per rank with the halo NCCL
+send / recv before every residual / colour pass inside it, ||f|| an NCCL
+allreduce -- paper_1608_01102_b200/slabs.py CSlabSolver, DESIGN.md §6.
 """
 
 import argparse
@@ -348,11 +349,11 @@ def main():
     slab = None
     if world > 1:
         from paper_1608_01102_b200 import slabs
-        slab, slab_states = slabs.build_lib_solver(spec, cfg, v0, vstar, [rank], world, w.N, w.dtype,
-                                                   comm=slabs.TorchComm())
+        slab, slab_states = slabs.build_c_solver(spec, cfg, v0, vstar, [rank], world, w.N, w.dtype,
+                                                 comm=slabs.NcclSlabComm())
         state = slab_states[0]
-        hier = slab.E[0].hier
-        n_local = slab.E[0].Nl
+        hier = slab                      # same profiling interface, summed over the local slabs
+        slab_t0, n_local = slab.frames[0]
     else:
         state = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
         hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
@@ -457,7 +458,10 @@ def main():
         if slab is None:
             d_in = list(vstar) + [t for t in (*state.V, state.PB, *state.U, state.P)]
         else:
-            d_in = list(slab.guides[0][0]) + [t for t in (*state.V, state.PB, *state.U, state.P)]
+            # this rank's guide frames v*_{t0} .. v*_{t0+n} (uploaded into the
+            # full guide tensor, re-bound by set_guide inside the timed region)
+            t1 = min(slab_t0 + n_local + 1, w.N)
+            d_in = [c[slab_t0:t1] for c in vstar] + [t for t in (*state.V, state.PB, *state.U, state.P)]
         d_st = [t for t in (*state.V, state.PB, *state.U, state.P)]
         h_in = [pin(t) for t in d_in]
         out_h = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_st]
@@ -479,6 +483,8 @@ def main():
                 d.copy_(h, non_blocking=True)
             if slab is None:
                 hier.set_guide(v0, vstar)
+            else:
+                slab.set_guide()
             step()
             for h, d in zip(out_h, d_st):
                 h.copy_(d, non_blocking=True)
@@ -551,6 +557,7 @@ def main():
         print(json.dumps(line), flush=True)
     hier.close()
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

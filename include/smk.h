@@ -229,6 +229,36 @@ int smk_nso_level_residual(smk_nso* h, int level, const smk_state* s, const void
 int smk_nso_level_color_pass(smk_nso* h, int level, int colour, const smk_state* s, const void* const vprev[],
                              const void* const unext[], const void* const vs[], const smk_residual* rhs,
                              void* stream);
+/* ---- time slabs in C++ (DESIGN.md §6): the whole slab V-cycle without host
+ * code per colour pass (replaces the per-level Python orchestration above on
+ * the product path; slabs.py CSlabSolver).  This process holds the
+ * contiguous slabs [first, first + n_local) of n_slabs (split_frames order:
+ * the first n_frames % n_slabs slabs one pair longer); prm->n_frames is the
+ * GLOBAL pair count.  Halos are refreshed before every residual and colour
+ * pass: local neighbours by device copies, the slabs of ranks rank - 1 /
+ * rank + 1 by NCCL send / recv (world > 1: nccl_id = the 128-byte
+ * ncclUniqueId of rank 0, from smk_nccl_unique_id, broadcast by the caller).
+ * The V-cycle (kernels, copies, NCCL P2P) is captured into one CUDA graph.
+ * states[k] holds local slab k's pairs (smk_slabs_frames). */
+typedef struct smk_slabs smk_slabs;
+int smk_nccl_unique_id(void* out, int nbytes);
+smk_slabs* smk_slabs_create(const smk_grid* g, const smk_nso_params* prm, int first, int n_local, int n_slabs,
+                            int rank, int world, const void* nccl_id);
+void smk_slabs_destroy(smk_slabs* h);
+int smk_slabs_levels(const smk_slabs* h);
+int64_t smk_slabs_device_bytes(const smk_slabs* h);
+int smk_slabs_frames(const smk_slabs* h, int local, int* t0, int* n_frames);
+/* v0: pinned initial velocity (1 frame); vstar: the full guide v*_0..v*_{N-1} */
+int smk_slabs_set_guide(smk_slabs* h, const void* const v0[], const void* const vstar[], void* stream);
+int smk_slabs_vcycle(smk_slabs* h, const smk_state* states, void* stream);
+int smk_slabs_gauge_fix(smk_slabs* h, const smk_state* states, void* stream);
+/* ||f||_inf / ||f||_2 over every slab of every rank (synchronising) */
+int smk_slabs_residual_norms(smk_slabs* h, const smk_state* states, double* res_inf, double* res_l2, void* stream);
+/* smk_nso_profile / _read_level summed over the local slabs (level < 0: all) */
+int smk_slabs_profile(smk_slabs* h, int enable);
+int smk_slabs_profile_read_level(smk_slabs* h, int kind, int level, double* ms, long long* launches,
+                                 long long* cell_timesteps);
+
 /* ---------------- advection optimisation (ao.py) ---------------- */
 
 /* One separable pass of the keyframe metric (GaussianMetric._filter,

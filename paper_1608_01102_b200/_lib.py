@@ -11,6 +11,8 @@ from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsmk.so")
+if os.environ.get("SMK_LIB_VARIANT"):   # tuning builds (build.py --variant), never the product default
+    LIB_PATH = os.path.join(HERE, f"libsmk_{os.environ['SMK_LIB_VARIANT']}.so")
 
 SMK_OK = 0
 SMK_NONCONVERGENCE = 1
@@ -109,6 +111,19 @@ SIGNATURES = {
     "smk_nso_level_color_pass": (I, [P, I, I, PS, P, P, P, PR, P]),
     "smk_axpby": (I, [I, P, P, D, D, I64, P]),
     "smk_axis_filter": (I, [I, I64, I, I64, P, I, D, D, P, P, P]),
+    "smk_nccl_unique_id": (I, [P, I]),
+    "smk_slabs_create": (P, [G, PP, I, I, I, I, I, P]),
+    "smk_slabs_destroy": (None, [P]),
+    "smk_slabs_levels": (I, [P]),
+    "smk_slabs_device_bytes": (I64, [P]),
+    "smk_slabs_frames": (I, [P, I, PI, PI]),
+    "smk_slabs_set_guide": (I, [P, P, P, P]),
+    "smk_slabs_vcycle": (I, [P, PS, P]),
+    "smk_slabs_gauge_fix": (I, [P, PS, P]),
+    "smk_slabs_residual_norms": (I, [P, PS, PD, PD, P]),
+    "smk_slabs_profile": (I, [P, I]),
+    "smk_slabs_profile_read_level": (I, [P, I, I, PD, ctypes.POINTER(ctypes.c_longlong),
+                                         ctypes.POINTER(ctypes.c_longlong)]),
 }
 
 _lib = None

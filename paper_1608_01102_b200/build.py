@@ -58,5 +58,22 @@ def build(force=False, verbose=True):
     return LIB
 
 
+def build_variant(name, defines):
+    """Tuning builds only: libsmk_<name>.so with extra -D flags on smk_stfas.cu
+    (loaded when SMK_LIB_VARIANT=<name>; the product library is libsmk.so)."""
+    build(verbose=False)
+    objdir = os.path.join(HERE, "build")
+    obj = os.path.join(objdir, f"smk_stfas_{name}.o")
+    cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + ["-c", os.path.join(CSRC, "smk_stfas.cu"), "-o", obj]
+    subprocess.check_call(cmd)
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES if s != "smk_stfas.cu"] + [obj]
+    out = os.path.join(HERE, f"libsmk_{name}.so")
+    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", out] + objs)
+    return out
+
+
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        build_variant(sys.argv[2], sys.argv[3:])
+    else:
+        build(force="--force" in sys.argv)

@@ -22,6 +22,10 @@
 #include <array>
 #include <type_traits>
 
+#include <dlfcn.h>
+#include <memory>
+#include <nccl.h>
+
 #include "smk_internal.cuh"
 
 namespace smk {
@@ -195,12 +199,28 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
 // upper wall face of the last cell along each axis (0 - rhs).  Neighbour
 // values come from the register caches (every V / U value the cell's faces
 // need is read once per thread, through L1).
-template <int DIM, bool PER, class R, bool HR, int NX>
-__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out) {
+// NORM (the stop test): the same values, not stored; each
+// block writes max |f| and sum f^2 (fp64) of its entries to part[2 blk ..],
+// reduced in a fixed order by k_norm_final -- every residual entry is
+// produced by exactly one thread, so this is ||f||_inf / ||f||_2 of the full
+// residual without writing it (5.4 GB at cfg5) and reading it back.
+template <int DIM, bool PER, class R, bool HR, int NX, bool NORM = false>
+__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out,
+                                             double* __restrict__ part = nullptr) {
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
   const int i = blockIdx.z;
+  R mx = R(0);
+  double sq = 0.0;
+  auto put = [&](R* dst, int64_t o, R v) {
+    if constexpr (NORM) {
+      mx = fmax(mx, rabs(v));
+      sq += (double)v * (double)v;
+    } else {
+      dst[o] = v;
+    }
+  };
   SMK_FRAME_LOOP(e, nc) {
     int c[3];
     ix.cell_idx32(e, c);
@@ -223,17 +243,65 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
       const int64_t o = (int64_t)i * cx.nf[k] + L.of[2 * k];
-      out.R3[k][o] = yu[2 * k];
-      out.R1[k][o] = yv[2 * k];
+      put(out.R3[k], o, yu[2 * k]);
+      put(out.R1[k], o, yv[2 * k]);
       if (!PER && wall[2 * k + 1]) {
         const int64_t ou = (int64_t)i * cx.nf[k] + L.of[2 * k + 1];
-        out.R3[k][ou] = HR ? R(0) - rhs.R3[k][ou] : R(0);
-        out.R1[k][ou] = HR ? R(0) - rhs.R1[k][ou] : R(0);
+        put(out.R3[k], ou, HR ? R(0) - rhs.R3[k][ou] : R(0));
+        put(out.R1[k], ou, HR ? R(0) - rhs.R1[k][ou] : R(0));
       }
     }
     const int64_t oc = (int64_t)i * nc + L.co;
-    out.R4[oc] = yu[NF];
-    out.R2[oc] = yv[NF];
+    put(out.R4, oc, yu[NF]);
+    put(out.R2, oc, yv[NF]);
+  }
+  if constexpr (NORM) {
+    __shared__ double shm[8], shs[8];
+    double m = warp_max((double)mx);
+    sq = warp_sum(sq);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+      shm[w] = m;
+      shs[w] = sq;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0, b = 0.0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+        a = fmax(a, shm[k]);
+        b += shs[k];
+      }
+      const int64_t blk = (int64_t)blockIdx.z * gridDim.x + blockIdx.x;
+      part[2 * blk] = a;
+      part[2 * blk + 1] = b;
+    }
+  }
+}
+
+// fixed-order reduction of the NORM blocks' partials: out = {max, sum}
+__global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ part, int64_t nblk, double* out) {
+  __shared__ double shm[32], shs[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t k = threadIdx.x; k < nblk; k += blockDim.x) {
+    a = fmax(a, part[2 * k]);
+    b += part[2 * k + 1];
+  }
+  a = warp_max(a);
+  b = warp_sum(b);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    shm[w] = a;
+    shs[w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      x = fmax(x, shm[k]);
+      y += shs[k];
+    }
+    out[0] = isnan(y) ? y : x;   // fmax drops NaN; the sum keeps it
+    out[1] = y;
   }
 }
 
@@ -245,8 +313,17 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
 // PIVOT selects partial pivoting (tournament row swaps, fully unrolled so the
 // arrays stay in registers); definite blocks use the natural order.
 template <class R, int B, int C, bool PIVOT>
+// (tiny is relative to the largest |entry| of A: scale-free SingularBlock test)
 __device__ __forceinline__ bool dense_solve(R (&A)[B][B], R (&X)[B][C], R tiny) {
   bool ok = true;
+  {
+    R amax = R(0);
+#pragma unroll
+    for (int r = 0; r < B; ++r)
+#pragma unroll
+      for (int c = 0; c < B; ++c) amax = fmax(amax, rabs(A[r][c]));
+    tiny *= amax;
+  }
   R inv[B];
 #pragma unroll
   for (int col = 0; col < B; ++col) {
@@ -306,13 +383,27 @@ __device__ __forceinline__ double pivot_rcp(double x) { return 1.0 / x; }
 // In-place LDL^T of a symmetric B x B matrix held in the lower triangle of T
 // (natural order, no pivoting -- used for the saddle blocks whose faces part
 // is positive definite): on exit T[r][c] (c < r) = L[r][c], dinv = 1 / d.
+//
+// SingularBlock ("block pivot below 1e-12"), made scale-free:
+// the blocks are K' = [[D~, g], [g^T, 0]], so a faces pivot is compared with
+// tiny * s (s = the largest diagonal of D~) and the saddle pivot, which has
+// units of |g|^2 / D~, with tiny * sigma / s (sigma = |g|^2).  tiny = 1e-12
+// in both precisions: in fp32 it flags breakdown (zero / denormal / NaN
+// pivots), in fp64 the SPEC's degenerate configurations too.
 template <class R, int B>
 __device__ __forceinline__ bool ldlt(R (&T)[B][B], R (&dinv)[B], R tiny) {
   bool ok = true;
+  R smax = R(0), sig = R(0);
+#pragma unroll
+  for (int k = 0; k < B - 1; ++k) {
+    smax = fmax(smax, rabs(T[k][k]));
+    sig += T[B - 1][k] * T[B - 1][k];
+  }
 #pragma unroll
   for (int col = 0; col < B; ++col) {
     const R piv = T[col][col];
-    if (!(rabs(piv) > tiny)) ok = false;
+    const R ref = col < B - 1 ? smax : sig / smax;
+    if (!(rabs(piv) > tiny * ref)) ok = false;
     dinv[col] = pivot_rcp(piv);
     R l[B];
 #pragma unroll
@@ -817,7 +908,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   // through Y = L^-1 [P M_{i+1}; 0]:  D~_{i+1} = D_{i+1} - Y^T diag(1/d) Y / dt^2,
   // and the back substitution needs W_i dv = K'^-1 [-P M_{i+1} dv / dt; 0],
   // so the pair hands off only D~_i and its rhs -- no explicit W.
-  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+  const R tinyv = R(1e-12);   // relative SingularBlock threshold (ldlt / dense_solve)
   // The dense block algebra below runs on lane pairs (columns 2h, 2h+1):
   // FFMA2 with a broadcast scalar in fp32, each lane rounded exactly like the
   // scalar FFMA of the same expression (same operand order, same summation
@@ -1051,8 +1142,13 @@ struct BackIn {
 // (so.V = the pass's output, cx.V its input): Vout = Vin + omega dv at every
 // face.  Same arithmetic as k_scgs_apply, so bitwise equal to the unfused
 // pass.
+// resident CTAs per SM the big-colour (compact) variant is register-capped
+// for (tuning builds: -DSMK_BACK_MINB=n)
+#ifndef SMK_BACK_MINB
+#define SMK_BACK_MINB 1
+#endif
 template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP, bool FUSE>
-__global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
+__global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
                                                    R* __restrict__ xout, StP<R> so) {
   using LN = Line<DIM>;
@@ -1066,7 +1162,7 @@ __global__ void __launch_bounds__(128) k_scgs_back(KktCtx<DIM, PER, R> cx, int o
   const auto& cg = lc.cg;
   const Loc<DIM, PER, NX> L(ix, cg.c);
   const R idt = cx.idt;
-  const R tinyv = sizeof(R) == 8 ? R(1e-300) : R(1e-30);
+  const R tinyv = R(1e-12);   // relative SingularBlock threshold (ldlt / dense_solve)
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
   // inputs of step i: hand-off of pair i; u-rows of pair i+1 and the V
   // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
@@ -1513,8 +1609,11 @@ struct Nso : NsoBase {
 
   // forward-kernel shape thresholds (colour cells): >= fwd_big -> TM 64 / P 1,
   // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
-  // overrides them (tuning runs only).
-  int64_t fwd_big = 148 * 64 * 4, fwd_mid = 148 * 32 * 2;
+  // overrides them (tuning runs only).  The 64^3 red-black colours (131,072
+  // cells: cfg5 level 1, cfg4 level 0) run TM 32 / P 2: 3.5 waves of TM 64
+  // CTAs left a half-empty last wave (level-1 forward 17.1 -> 12.6 ms per
+  // cfg5 V-cycle, backward 6.4 -> 5.3 ms with the factored hand-off).
+  int64_t fwd_big = 148 * 64 * 16, fwd_mid = 148 * 32 * 2;
   // backward: colours with >= back_flat cells use the unpipelined variant
   // (occupancy), smaller ones the load-pipelined one.  SMK_BACK_FLAT overrides.
   int64_t back_flat = 148 * 128 * 4;
@@ -2057,31 +2156,58 @@ struct Nso : NsoBase {
     return cuda_check("nso_gauge");
   }
 
+  // ||f||_inf and ||f||_2 of the level-0 residual: one fused residual+norm
+  // launch (k_kkt<NORM>, nothing stored), a fixed-order final reduction and
+  // one read-back together with the SingularBlock flag
+  double* nparts = nullptr;
+  int64_t nparts_n = 0;
+  // launch the fused residual + norm of level 0 (halos as set) and its
+  // fixed-order reduction into dev_out[0..1] = {max |f|, sum f^2}
+  int norm_launch(const StP<R>& top, double* dev_out, cudaStream_t st) {
+    auto c = ctx(0, top);
+    const dim3 grid = frame_grid(lv[0].nc, prm.n_frames, 256);
+    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    if (nparts_n < nblk + 1) {
+      nparts = (double*)mem.get(sizeof(double) * 2 * (nblk + 1));
+      if (!nparts) { nparts_n = 0; set_error("nso: out of device memory (norm partials)"); return SMK_ERR_CUDA; }
+      nparts_n = nblk + 1;
+    }
+    prof_begin(2, 0, lv[0].nc, st);
+    with_nx(0, [&](auto nxc) {
+      constexpr int NXv = decltype(nxc)::value;
+      k_kkt<DIM, PER, R, false, NXv, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts);
+    });
+    count_launch();
+    prof_end(2, st);
+    k_norm_final<<<1, 1024, 0, st>>>(nparts, nblk, dev_out ? dev_out : nparts + 2 * nblk);
+    count_launch();
+    return SMK_OK;
+  }
+  // read the SingularBlock flag after a synchronisation point
+  int take_flag(int fl, cudaStream_t st) {
+    if (fl) {
+      cudaMemsetAsync(flag, 0, sizeof(int), st);
+      set_error("SCGS block pivot below threshold (SingularBlock)");
+      return SMK_SINGULAR_BLOCK;
+    }
+    return SMK_OK;
+  }
   int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) override {
     if (!guide_set) { set_error("nso: set_guide not called"); return SMK_ERR_ARG; }
-    StP<R> top = from_api(s);
-    const Level<R>& L = lv[0];
-    residual(0, top, nullptr, L.f, st);
-    const int N = prm.n_frames;
-    int dt = sizeof(R) == 8 ? SMK_F64 : SMK_F32;
-    double m = 0.0, q = 0.0;
-    for (int k = 0; k < DIM; ++k) {
-      m = std::max(m, host_absmax(dt, L.f.R1[k], (int64_t)N * L.nf[k], st, scal));
-      m = std::max(m, host_absmax(dt, L.f.R3[k], (int64_t)N * L.nf[k], st, scal));
-      if (r2) {
-        q += host_sum(dt, L.f.R1[k], L.f.R1[k], (int64_t)N * L.nf[k], st, parts);
-        q += host_sum(dt, L.f.R3[k], L.f.R3[k], (int64_t)N * L.nf[k], st, parts);
-      }
-    }
-    m = std::max(m, host_absmax(dt, L.f.R2, (int64_t)N * L.nc, st, scal));
-    m = std::max(m, host_absmax(dt, L.f.R4, (int64_t)N * L.nc, st, scal));
-    if (r2) {
-      q += host_sum(dt, L.f.R2, L.f.R2, (int64_t)N * L.nc, st, parts);
-      q += host_sum(dt, L.f.R4, L.f.R4, (int64_t)N * L.nc, st, parts);
-      *r2 = std::sqrt(q);
-    }
-    *ri = m;
-    return check_flag(st);
+    int rc = norm_launch(from_api(s), nullptr, st);
+    if (rc) return rc;
+    const dim3 grid = frame_grid(lv[0].nc, prm.n_frames, 256);
+    const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
+    double h[2] = {0.0, 0.0};
+    int fl = 0;
+    cudaMemcpyAsync(h, nparts + 2 * nblk, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&fl, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    rc = cuda_check("nso_norms");
+    if (rc) return rc;
+    *ri = h[0];
+    if (r2) *r2 = std::sqrt(h[1]);
+    return take_flag(fl, st);
   }
 
   // ---- slab (per-level) API: caller owns the level's state and halos ----
@@ -2144,6 +2270,450 @@ struct Nso : NsoBase {
     }
     sweep(0, top, rhs ? &r : nullptr, st);
     return check_flag(st);
+  }
+};
+
+
+// ---------------------------------------------------------------------------
+// Time slabs: this process's contiguous slabs of the spacetime
+// volume, each an Nso over its pairs (t0, n_total set), driven through the
+// whole FAS V-cycle in C++ with the slab halos refreshed before every
+// residual and every colour pass -- local neighbours by device copies,
+// remote ones (the ranks holding the slabs on either side) by NCCL
+// send / recv on the same stream.  The V-cycle (kernels, copies and NCCL
+// P2P) is captured once into a CUDA graph and replayed; no host code runs
+// per colour pass.  NCCL is loaded with dlopen on first use (world > 1).
+// ---------------------------------------------------------------------------
+struct NcclApi {
+  void* so = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*ErrStr)(ncclResult_t) = nullptr;
+  bool load() {
+    if (so) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names)
+      if ((so = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!so) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(so, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(so, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(so, "ncclCommDestroy");
+    GroupStart = (decltype(GroupStart))dlsym(so, "ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))dlsym(so, "ncclGroupEnd");
+    Send = (decltype(Send))dlsym(so, "ncclSend");
+    Recv = (decltype(Recv))dlsym(so, "ncclRecv");
+    AllReduce = (decltype(AllReduce))dlsym(so, "ncclAllReduce");
+    ErrStr = (decltype(ErrStr))dlsym(so, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && CommDestroy && GroupStart && GroupEnd && Send && Recv && AllReduce;
+  }
+};
+static NcclApi g_nccl;
+
+struct SlabsBase {
+  virtual ~SlabsBase() {}
+  virtual int set_guide(const void* const v0[], const void* const vstar[], cudaStream_t st) = 0;
+  virtual int vcycle(const smk_state* s, cudaStream_t st) = 0;
+  virtual int gauge(const smk_state* s, cudaStream_t st) = 0;
+  virtual int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) = 0;
+  virtual int levels() const = 0;
+  virtual int64_t bytes() const = 0;
+  virtual int frames(int k, int* t0, int* n) const = 0;
+  virtual int profile(int enable) = 0;
+  virtual int profile_read(int kind, int level, double* ms, long long* launches, long long* cells) = 0;
+};
+
+template <int DIM, bool PER, class R>
+struct Slabs : SlabsBase {
+  using NS = Nso<DIM, PER, R>;
+  int first, nloc, nslab, rank, world, ntot;
+  std::vector<std::unique_ptr<NS>> E;
+  std::vector<int> t0s, ns;
+  int L = 0;
+  Scratch mem;
+  int64_t nbytes = 0;
+  ncclComm_t comm = nullptr;
+  // per level: pinned v0 (slab 0), per local slab: halo frames and guide
+  struct H {
+    R* vprev[3] = {nullptr, nullptr, nullptr};
+    R* unext[3] = {nullptr, nullptr, nullptr};
+    R* vs[3] = {nullptr, nullptr, nullptr};
+  };
+  std::vector<std::array<R*, 3>> v0l;
+  std::vector<std::vector<H>> hl;   // [level][local slab]
+  double* dnorm = nullptr;           // per local slab {max, sum}, then the combined pair
+  bool ok = true, guide_set = false;
+
+  R* alloc(int64_t n) {
+    void* p = mem.get((size_t)n * sizeof(R));
+    if (!p) { ok = false; return nullptr; }
+    cudaMemset(p, 0, (size_t)n * sizeof(R));
+    nbytes += n * (int64_t)sizeof(R);
+    return (R*)p;
+  }
+
+  Slabs(const Geo& g, const smk_nso_params& p, int first_, int nloc_, int nslab_, int rank_, int world_,
+        const void* nccl_id)
+      : first(first_), nloc(nloc_), nslab(nslab_), rank(rank_), world(world_), ntot(p.n_frames) {
+    // split_frames (slabs.py): contiguous, the first (ntot % nslab) slabs one longer
+    const int base = ntot / nslab, extra = ntot % nslab;
+    int t = 0;
+    for (int q = 0; q < nslab; ++q) {
+      const int n = base + (q < extra ? 1 : 0);
+      if (q >= first && q < first + nloc) {
+        t0s.push_back(t);
+        ns.push_back(n);
+      }
+      t += n;
+    }
+    for (int k = 0; k < nloc; ++k) {
+      smk_nso_params q = p;
+      q.t0 = t0s[k];
+      q.n_frames = ns[k];
+      q.n_total = ntot;
+      E.emplace_back(new NS(g, q));
+      if (!E.back()->ok) ok = false;
+      nbytes += E.back()->bytes();
+    }
+    if (!ok) return;
+    L = E[0]->levels();
+    v0l.resize(L);
+    hl.assign(L, std::vector<H>(nloc));
+    for (int l = 0; l < L; ++l) {
+      const auto& Lv = E[0]->lv[l];
+      for (int c = 0; c < 3; ++c) v0l[l][c] = c < DIM ? alloc(Lv.nf[c]) : nullptr;
+      for (int k = 0; k < nloc; ++k)
+        for (int c = 0; c < DIM; ++c) {
+          hl[l][k].vprev[c] = alloc(Lv.nf[c]);
+          hl[l][k].unext[c] = alloc(Lv.nf[c]);
+          hl[l][k].vs[c] = alloc((int64_t)(ns[k] + 1) * Lv.nf[c]);
+        }
+    }
+    dnorm = (double*)mem.get(sizeof(double) * 2 * (nloc + 1));
+    if (!dnorm) ok = false;
+    if (world > 1) {
+      if (!nccl_id || !g_nccl.load()) {
+        set_error("slabs: world > 1 needs NCCL (libnccl.so.2) and a unique id");
+        ok = false;
+        return;
+      }
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof(id));
+      if (g_nccl.CommInitRank(&comm, world, id, rank) != ncclSuccess) {
+        set_error("slabs: ncclCommInitRank failed");
+        comm = nullptr;
+        ok = false;
+      }
+    }
+  }
+  ~Slabs() override {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (cap) cudaStreamDestroy(cap);
+    if (comm) g_nccl.CommDestroy(comm);
+  }
+  int levels() const override { return L; }
+  int64_t bytes() const override { return nbytes; }
+  int frames(int k, int* t0, int* n) const override {
+    if (k < 0 || k >= nloc) { set_error("bad local slab"); return SMK_ERR_ARG; }
+    *t0 = t0s[k];
+    *n = ns[k];
+    return SMK_OK;
+  }
+  bool global_first(int k) const { return first + k == 0; }
+  bool global_last(int k) const { return first + k == nslab - 1; }
+
+  // vstar: the full guide v*_0 .. v*_{ntot-1} (ntot frames); each slab keeps
+  // v*_{t0} .. v*_{t0+n} per level (the frame past the global end is zero)
+  int set_guide(const void* const v0[], const void* const vstar[], cudaStream_t st) override {
+    const auto& L0 = E[0]->lv[0];
+    for (int c = 0; c < DIM; ++c)
+      cudaMemcpyAsync(v0l[0][c], v0[c], (size_t)L0.nf[c] * sizeof(R), cudaMemcpyDeviceToDevice, st);
+    for (int k = 0; k < nloc; ++k)
+      for (int c = 0; c < DIM; ++c) {
+        const int nfr = std::min(ns[k] + 1, ntot - t0s[k]);
+        cudaMemcpyAsync(hl[0][k].vs[c], (const R*)vstar[c] + (int64_t)t0s[k] * L0.nf[c],
+                        (size_t)nfr * L0.nf[c] * sizeof(R), cudaMemcpyDeviceToDevice, st);
+        if (nfr < ns[k] + 1)
+          cudaMemsetAsync(hl[0][k].vs[c] + (int64_t)nfr * L0.nf[c], 0,
+                          (size_t)(ns[k] + 1 - nfr) * L0.nf[c] * sizeof(R), st);
+      }
+    for (int l = 1; l < L; ++l) {
+      const Geo& gf = E[0]->lv[l - 1].g;
+      Face3<R> a;
+      FaceW<R> oa;
+      for (int c = 0; c < 3; ++c) { a.c[c] = v0l[l - 1][c]; oa.c[c] = v0l[l][c]; }
+      launch_restrict_face<DIM, PER, R>(gf, 1, a, oa, st);
+      for (int k = 0; k < nloc; ++k) {
+        for (int c = 0; c < 3; ++c) { a.c[c] = hl[l - 1][k].vs[c]; oa.c[c] = hl[l][k].vs[c]; }
+        launch_restrict_face<DIM, PER, R>(gf, ns[k] + 1, a, oa, st);
+      }
+    }
+    // the slab Nso's never use their own guide buffers (halo mode), but their
+    // entry points check that a guide was bound
+    for (auto& e : E) e->guide_set = true;
+    guide_set = true;
+    return cuda_check("slabs_set_guide");
+  }
+
+  // halos of level l from the local slabs' current states (V read from sv[k],
+  // U from su[k]); remote neighbours over NCCL
+  void exchange(int l, const std::vector<StP<R>>& sv, cudaStream_t st) {
+    const auto& Lv = E[0]->lv[l];
+    for (int k = 0; k < nloc; ++k) {
+      if (k > 0)
+        for (int c = 0; c < DIM; ++c)
+          cudaMemcpyAsync(hl[l][k].vprev[c], sv[k - 1].V[c] + (int64_t)(ns[k - 1] - 1) * Lv.nf[c],
+                          (size_t)Lv.nf[c] * sizeof(R), cudaMemcpyDeviceToDevice, st);
+      if (k < nloc - 1)
+        for (int c = 0; c < DIM; ++c)
+          cudaMemcpyAsync(hl[l][k].unext[c], sv[k + 1].U[c], (size_t)Lv.nf[c] * sizeof(R), cudaMemcpyDeviceToDevice,
+                          st);
+    }
+    if (world > 1 && comm) {
+      const ncclDataType_t ty = sizeof(R) == 8 ? ncclFloat64 : ncclFloat32;
+      g_nccl.GroupStart();
+      if (!global_first(0))   // left neighbour: send my first U frame, receive its last V frame
+        for (int c = 0; c < DIM; ++c) {
+          g_nccl.Send(sv[0].U[c], (size_t)Lv.nf[c], ty, rank - 1, comm, st);
+          g_nccl.Recv(hl[l][0].vprev[c], (size_t)Lv.nf[c], ty, rank - 1, comm, st);
+        }
+      if (!global_last(nloc - 1))
+        for (int c = 0; c < DIM; ++c) {
+          g_nccl.Send(sv[nloc - 1].V[c] + (int64_t)(ns[nloc - 1] - 1) * Lv.nf[c], (size_t)Lv.nf[c], ty, rank + 1,
+                      comm, st);
+          g_nccl.Recv(hl[l][nloc - 1].unext[c], (size_t)Lv.nf[c], ty, rank + 1, comm, st);
+        }
+      g_nccl.GroupEnd();
+    }
+  }
+  void bind(int l, int k) {
+    const void* vp[3] = {nullptr, nullptr, nullptr};
+    const void* un[3] = {nullptr, nullptr, nullptr};
+    const void* vs[3] = {nullptr, nullptr, nullptr};
+    for (int c = 0; c < DIM; ++c) {
+      vp[c] = global_first(k) ? (const void*)v0l[l][c] : (const void*)hl[l][k].vprev[c];
+      un[c] = hl[l][k].unext[c];
+      vs[c] = hl[l][k].vs[c];
+    }
+    E[k]->set_halo(vp, global_last(k) ? nullptr : un, vs);
+  }
+  void unbind(int k) { E[k]->use_halo = false; }
+
+  void sweep(int l, const std::vector<StP<R>>& S, const std::vector<const ResP<R>*>& rhs, cudaStream_t st) {
+    NS& e0 = *E[0];
+    if (e0.fusable(l) && e0.n_colors() == 2) {
+      std::vector<StP<R>> alt = S;
+      for (int k = 0; k < nloc; ++k)
+        for (int c = 0; c < 3; ++c) alt[k].V[c] = E[k]->vswap[l][c];
+      exchange(l, S, st);
+      for (int k = 0; k < nloc; ++k) {
+        bind(l, k);
+        E[k]->color_pass(l, 0, S[k], rhs[k], st, &alt[k]);
+        unbind(k);
+      }
+      exchange(l, alt, st);
+      for (int k = 0; k < nloc; ++k) {
+        bind(l, k);
+        E[k]->color_pass(l, 1, alt[k], rhs[k], st, &S[k]);
+        unbind(k);
+      }
+      return;
+    }
+    for (int col = 0; col < e0.n_colors(); ++col) {
+      exchange(l, S, st);
+      for (int k = 0; k < nloc; ++k) {
+        bind(l, k);
+        E[k]->color_pass(l, col, S[k], rhs[k], st);
+        unbind(k);
+      }
+    }
+  }
+  void residual(int l, const std::vector<StP<R>>& S, const std::vector<const ResP<R>*>& rhs,
+                const std::vector<ResP<R>>& out, cudaStream_t st) {
+    exchange(l, S, st);
+    for (int k = 0; k < nloc; ++k) {
+      bind(l, k);
+      E[k]->residual(l, S[k], rhs[k], out[k], st);
+      unbind(k);
+    }
+  }
+  void vcycle_level(int l, const std::vector<StP<R>>& S, const std::vector<const ResP<R>*>& rhs, cudaStream_t st) {
+    const int n1 = E[0]->prm.nu1, n2 = E[0]->prm.nu2, nc = E[0]->prm.n_coarse;
+    if (l == L - 1) {
+      for (int it = 0; it < nc; ++it) sweep(l, S, rhs, st);
+      return;
+    }
+    for (int it = 0; it < n1; ++it) sweep(l, S, rhs, st);
+    std::vector<StP<R>> C(nloc);
+    std::vector<ResP<R>> F(nloc), CF(nloc), CR(nloc);
+    std::vector<const ResP<R>*> cfp(nloc), crp(nloc);
+    for (int k = 0; k < nloc; ++k) {
+      auto& ck = E[k]->lv[l + 1];
+      C[k] = ck.st;
+      F[k] = E[k]->lv[l].f;
+      CF[k] = ck.f;
+      CR[k] = ck.rhs;
+      cfp[k] = &E[k]->lv[l + 1].f;
+      crp[k] = &E[k]->lv[l + 1].rhs;
+      E[k]->restrict_state(l, S[k], ck.st, st);
+      E[k]->copy_state(l + 1, ck.st, ck.st0, st);
+    }
+    residual(l, S, rhs, F, st);
+    for (int k = 0; k < nloc; ++k) E[k]->restrict_res(l, F[k], CF[k], st);
+    residual(l + 1, C, cfp, CR, st);
+    vcycle_level(l + 1, C, crp, st);
+    for (int k = 0; k < nloc; ++k) {
+      auto& ck = E[k]->lv[l + 1];
+      E[k]->axpby_state(l + 1, ck.st, ck.st0, 1.0, -1.0, st);
+      E[k]->prolong_add(l + 1, ck.st0, S[k], st);
+    }
+    for (int it = 0; it < n2; ++it) sweep(l, S, rhs, st);
+  }
+
+  std::vector<StP<R>> tops(const smk_state* s) const {
+    std::vector<StP<R>> S(nloc);
+    for (int k = 0; k < nloc; ++k) S[k] = NS::from_api(&s[k]);
+    return S;
+  }
+  // graph of the whole slab V-cycle (re-captured when a state pointer changes)
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  std::vector<const void*> key;
+  long long exec_launches = 0;
+  bool graph_ok = getenv("SMK_NO_GRAPH") == nullptr;
+
+  // per-kernel CUDA-event profile summed over the local slabs (launched
+  // directly, not from the graph, while enabled -- like Nso)
+  bool prof = false;
+  int profile(int enable) override {
+    prof = enable != 0;
+    for (auto& e : E) e->profile(enable);
+    return SMK_OK;
+  }
+  int profile_read(int kind, int level, double* ms, long long* launches, long long* cells) override {
+    double t = 0.0;
+    long long n = 0, c = 0;
+    for (auto& e : E) {
+      double a = 0.0;
+      long long b = 0, d = 0;
+      int rc = e->profile_read(kind, level, &a, &b, &d);
+      if (rc) return rc;
+      t += a;
+      n += b;
+      c += d;
+    }
+    if (ms) *ms = t;
+    if (launches) *launches = n;
+    if (cells) *cells = c;
+    return SMK_OK;
+  }
+
+  int vcycle(const smk_state* s, cudaStream_t st) override {
+    if (!guide_set) { set_error("slabs: set_guide not called"); return SMK_ERR_ARG; }
+    const auto S = tops(s);
+    const std::vector<const ResP<R>*> none(nloc, nullptr);
+    if (!graph_ok || prof) {
+      vcycle_level(0, S, none, st);
+      return cuda_check("slabs_vcycle");
+    }
+    std::vector<const void*> kk;
+    for (int k = 0; k < nloc; ++k) {
+      for (int c = 0; c < 3; ++c) { kk.push_back(s[k].V[c]); kk.push_back(s[k].U[c]); }
+      kk.push_back(s[k].P);
+      kk.push_back(s[k].PB);
+    }
+    if (!exec || kk != key) {
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+      if (!cap && cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        graph_ok = false;
+        return vcycle(s, st);
+      }
+      // the capture stream must see the caller's prior work
+      cudaEvent_t ev;
+      cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      cudaEventRecord(ev, st);
+      cudaStreamWaitEvent(cap, ev, 0);
+      cudaEventDestroy(ev);
+      const long long n0 = launch_count();
+      cudaGraph_t g = nullptr;
+      bool okc = cudaStreamBeginCapture(cap, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+      if (okc) vcycle_level(0, S, none, cap);
+      okc = okc && cudaStreamEndCapture(cap, &g) == cudaSuccess && g;
+      okc = okc && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
+      if (g) cudaGraphDestroy(g);
+      if (!okc) {
+        cudaGetLastError();
+        exec = nullptr;
+        graph_ok = false;
+        return vcycle(s, st);
+      }
+      exec_launches = launch_count() - n0;
+      key = kk;
+    } else {
+      count_launch((int)exec_launches);
+    }
+    cudaGraphLaunch(exec, st);
+    return cuda_check("slabs_vcycle");
+  }
+  int gauge(const smk_state* s, cudaStream_t st) override {
+    for (int k = 0; k < nloc; ++k) {
+      int rc = E[k]->gauge(&s[k], st);
+      if (rc) return rc;
+    }
+    return SMK_OK;
+  }
+  int norms(const smk_state* s, double* ri, double* r2, cudaStream_t st) override {
+    if (!guide_set) { set_error("slabs: set_guide not called"); return SMK_ERR_ARG; }
+    const auto S = tops(s);
+    exchange(0, S, st);
+    for (int k = 0; k < nloc; ++k) {
+      bind(0, k);
+      int rc = E[k]->norm_launch(S[k], dnorm + 2 * k, st);
+      unbind(k);
+      if (rc) return rc;
+    }
+    std::vector<double> h(2 * nloc);
+    std::vector<int> fl(nloc, 0);
+    cudaMemcpyAsync(h.data(), dnorm, sizeof(double) * 2 * nloc, cudaMemcpyDeviceToHost, st);
+    for (int k = 0; k < nloc; ++k) cudaMemcpyAsync(&fl[k], E[k]->flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int rc = cuda_check("slabs_norms");
+    if (rc) return rc;
+    double mx = 0.0, sq = 0.0;
+    for (int k = 0; k < nloc; ++k) {
+      mx = std::isnan(h[2 * k + 1]) ? h[2 * k + 1] : std::max(mx, h[2 * k]);
+      sq += h[2 * k + 1];
+    }
+    if (world > 1 && comm) {
+      double both[2] = {mx, sq};
+      double* d = dnorm + 2 * nloc;
+      cudaMemcpyAsync(d, both, sizeof(both), cudaMemcpyHostToDevice, st);
+      g_nccl.GroupStart();
+      g_nccl.AllReduce(d, d, 1, ncclFloat64, ncclMax, comm, st);
+      g_nccl.AllReduce(d + 1, d + 1, 1, ncclFloat64, ncclSum, comm, st);
+      g_nccl.GroupEnd();
+      cudaMemcpyAsync(both, d, sizeof(both), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      rc = cuda_check("slabs_norms_allreduce");
+      if (rc) return rc;
+      mx = both[0];
+      sq = both[1];
+    }
+    *ri = mx;
+    if (r2) *r2 = std::sqrt(sq);
+    for (int k = 0; k < nloc; ++k) {
+      rc = E[k]->take_flag(fl[k], st);
+      if (rc) return rc;
+    }
+    return SMK_OK;
   }
 };
 
@@ -2210,7 +2780,86 @@ static NsoBase* make_nso(const smk_grid* g, const smk_nso_params* p) {
   return out;
 }
 
+struct smk_slabs {
+  SlabsBase* impl;
+};
+
 extern "C" {
+
+int smk_nccl_unique_id(void* out, int nbytes) {
+  if (!out || nbytes < (int)sizeof(ncclUniqueId)) { set_error("need %d bytes", (int)sizeof(ncclUniqueId)); return SMK_ERR_ARG; }
+  if (!g_nccl.load()) { set_error("libnccl.so.2 not found"); return SMK_ERR_CUDA; }
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) { set_error("ncclGetUniqueId failed"); return SMK_ERR_CUDA; }
+  memcpy(out, &id, sizeof(id));
+  return SMK_OK;
+}
+
+smk_slabs* smk_slabs_create(const smk_grid* g, const smk_nso_params* p, int first, int n_local, int n_slabs, int rank,
+                            int world, const void* nccl_id) {
+  if (check_grid(g) || check_params(p) || check_colouring(g, p)) return nullptr;
+  if (p->t0 != 0 || (p->n_total != 0 && p->n_total != p->n_frames)) {
+    set_error("slabs: n_frames is the global pair count (t0 = 0, n_total = 0)");
+    return nullptr;
+  }
+  if (n_slabs < 1 || n_slabs > p->n_frames || first < 0 || n_local < 1 || first + n_local > n_slabs || world < 1 ||
+      rank < 0 || rank >= world) {
+    set_error("slabs: bad slab range / rank");
+    return nullptr;
+  }
+  SlabsBase* impl = nullptr;
+  dispatch(g, [&](auto tag) {
+    using T = decltype(tag);
+    auto* s = new Slabs<T::DIM, T::PER, typename T::R>(to_geo(g), *p, first, n_local, n_slabs, rank, world, nccl_id);
+    if (!s->ok) {
+      delete s;
+      return SMK_ERR_CUDA;
+    }
+    impl = s;
+    return SMK_OK;
+  });
+  if (!impl) return nullptr;
+  return new smk_slabs{impl};
+}
+
+void smk_slabs_destroy(smk_slabs* h) {
+  if (!h) return;
+  cudaDeviceSynchronize();
+  delete h->impl;
+  delete h;
+}
+
+int smk_slabs_levels(const smk_slabs* h) { return h ? h->impl->levels() : 0; }
+int64_t smk_slabs_device_bytes(const smk_slabs* h) { return h ? h->impl->bytes() : 0; }
+int smk_slabs_frames(const smk_slabs* h, int k, int* t0, int* n) {
+  if (!h || !t0 || !n) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->frames(k, t0, n);
+}
+int smk_slabs_set_guide(smk_slabs* h, const void* const v0[], const void* const vstar[], void* stream) {
+  if (!h || !v0 || !vstar) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->set_guide(v0, vstar, (cudaStream_t)stream);
+}
+int smk_slabs_vcycle(smk_slabs* h, const smk_state* states, void* stream) {
+  if (!h || !states) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->vcycle(states, (cudaStream_t)stream);
+}
+int smk_slabs_gauge_fix(smk_slabs* h, const smk_state* states, void* stream) {
+  if (!h || !states) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->gauge(states, (cudaStream_t)stream);
+}
+int smk_slabs_residual_norms(smk_slabs* h, const smk_state* states, double* ri, double* r2, void* stream) {
+  if (!h || !states || !ri) { set_error("null argument"); return SMK_ERR_ARG; }
+  return h->impl->norms(states, ri, r2, (cudaStream_t)stream);
+}
+int smk_slabs_profile(smk_slabs* h, int enable) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->profile(enable);
+}
+int smk_slabs_profile_read_level(smk_slabs* h, int kind, int level, double* ms, long long* launches,
+                                 long long* cells) {
+  if (!h) { set_error("null handle"); return SMK_ERR_ARG; }
+  return h->impl->profile_read(kind, level, ms, launches, cells);
+}
 
 smk_nso* smk_nso_create(const smk_grid* g, const smk_nso_params* p) {
   if (check_grid(g) || check_params(p) || check_colouring(g, p)) return nullptr;

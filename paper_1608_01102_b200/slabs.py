@@ -215,6 +215,11 @@ class SlabSolver:
         for e, st in zip(self.E, states):
             e.gauge(st)
 
+    def close(self):
+        for e in self.E:
+            if hasattr(e, "hier"):
+                e.hier.close()
+
     def solve(self, states, eps=1e-5, relative=False, cycle_budget=50):
         ri, r2 = self.norms(states)
         hist = [(0, ri, r2)]
@@ -384,3 +389,135 @@ def build_lib_solver(spec, cfg, v0, vstar, slab_ids, n_slabs, n_total, dtype=tor
     states = [e.zeros_state() for e in engines]
     solver = SlabSolver(engines, slab_ids, n_slabs, v0_levels, guides, comm, cfg.nu1, cfg.nu2, cfg.n_coarse)
     return solver, states
+
+
+# ---------------------------------------------------------------------------
+# the product path: the slab V-cycle in C++ (smk_slabs_*, one CUDA graph per
+# V-cycle with the halo copies / NCCL P2P inside; no Python per colour pass)
+# ---------------------------------------------------------------------------
+
+
+class NcclSlabComm:
+    """Rank layout of the C++ slab set: world ranks, rank r holds a contiguous
+    block of slabs; the NCCL communicator is created inside libsmk from rank
+    0's unique id, broadcast here over torch.distributed (any backend)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if self.rank == 0:
+            raw = (ctypes.c_ubyte * 128)()
+            _lib.check(_lib.load().smk_nccl_unique_id(ctypes.cast(raw, ctypes.c_void_p), 128), "nccl_unique_id")
+            buf = torch.tensor(list(raw), dtype=torch.uint8)
+        dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        b = buf.to(dev)
+        dist.broadcast(b, 0, group=group)
+        self.uid = bytes(b.cpu().tolist())
+
+
+class CSlabSolver:
+    """Time-slab STFAS on libsmk's C++ slab set: same phases
+    and halo semantics as SlabSolver (bitwise the same kernels per slab), the
+    whole V-cycle replayed from one CUDA graph."""
+
+    def __init__(self, spec, cfg, v0, vstar, slab_ids, n_slabs, n_total, dtype=torch.float64, comm=None):
+        _dev.require_device()
+        self.dtype = dtype
+        self.spec = spec
+        self.ids = list(slab_ids)
+        if self.ids != list(range(self.ids[0], self.ids[0] + len(self.ids))):
+            raise ValueError("local slabs must be contiguous")
+        self._L = _lib.load()
+        rank, world, uid = 0, 1, None
+        if comm is not None:
+            rank, world, uid = comm.rank, comm.world, comm.uid
+        self._uid = ctypes.create_string_buffer(uid, 128) if uid else None
+        g = _dev.grid(spec, dtype)
+        p = cfg.params(n_total)
+        h = self._L.smk_slabs_create(ctypes.byref(g), ctypes.byref(p), self.ids[0], len(self.ids), n_slabs, rank,
+                                     world, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None)
+        if not h:
+            _lib.check(_lib.SMK_ERR_CUDA, "slabs_create")
+        self._h = h
+        self.L = self._L.smk_slabs_levels(h)
+        self.frames = []
+        for k in range(len(self.ids)):
+            t0, n = ctypes.c_int(), ctypes.c_int()
+            _lib.check(self._L.smk_slabs_frames(h, k, ctypes.byref(t0), ctypes.byref(n)), "slabs_frames")
+            self.frames.append((t0.value, n.value))
+        self.set_guide(v0, vstar)
+
+    def set_guide(self, v0=None, vstar=None):
+        """Bind v0 / the full guide v*_0..v*_{N-1} (device copies kept); with
+        no arguments, re-read the bound tensors (after an in-place update)."""
+        if v0 is not None:
+            self._v0 = tuple(_dev.as_dev(c, self.dtype).contiguous() for c in v0)
+        if vstar is not None:
+            self._vs = tuple(_dev.as_dev(c, self.dtype).contiguous() for c in vstar)
+        _lib.check(self._L.smk_slabs_set_guide(self._h, _lib.ptrs(self._v0), _lib.ptrs(self._vs), _dev.stream()),
+                   "slabs_set_guide")
+
+    def zero_states(self):
+        return [SpacetimeState.zeros(self.spec, n, self.dtype) for _, n in self.frames]
+
+    def _arr(self, states):
+        arr = (_lib.smk_state * len(states))()
+        for k, st in enumerate(states):
+            arr[k] = st.c_struct()
+        return arr
+
+    def vcycle(self, states):
+        _lib.check(self._L.smk_slabs_vcycle(self._h, self._arr(states), _dev.stream()), "slabs_vcycle")
+        return states
+
+    def gauge(self, states):
+        _lib.check(self._L.smk_slabs_gauge_fix(self._h, self._arr(states), _dev.stream()), "slabs_gauge")
+
+    def norms(self, states):
+        ri, r2 = ctypes.c_double(), ctypes.c_double()
+        _lib.check(self._L.smk_slabs_residual_norms(self._h, self._arr(states), ctypes.byref(ri), ctypes.byref(r2),
+                                                    _dev.stream()), "slabs_norms")
+        return ri.value, r2.value
+
+    def solve(self, states, eps=1e-5, relative=False, cycle_budget=50):
+        return SlabSolver.solve(self, states, eps, relative, cycle_budget)
+
+    def device_bytes(self):
+        return int(self._L.smk_slabs_device_bytes(self._h))
+
+    # the StfasHierarchy profiling interface, summed over the local slabs
+    KERNELS = StfasHierarchy.KERNELS
+
+    @property
+    def levels(self):
+        return self.L
+
+    def profile(self, enable=True):
+        _lib.check(self._L.smk_slabs_profile(self._h, int(bool(enable))), "slabs_profile")
+
+    def profile_read(self, kind=0, level=None):
+        ms, n, cells = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_longlong()
+        _lib.check(self._L.smk_slabs_profile_read_level(self._h, int(kind), -1 if level is None else int(level),
+                                                        ctypes.byref(ms), ctypes.byref(n), ctypes.byref(cells)),
+                   "slabs_profile_read")
+        return ms.value, n.value, cells.value
+
+    def close(self):
+        if self._h:
+            self._L.smk_slabs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_c_solver(spec, cfg, v0, vstar, slab_ids, n_slabs, n_total, dtype=torch.float64, comm=None):
+    """C++ slab solver for the local slabs `slab_ids` of `n_slabs`, and zero
+    states for them."""
+    s = CSlabSolver(spec, cfg, v0, vstar, slab_ids, n_slabs, n_total, dtype, comm)
+    return s, s.zero_states()

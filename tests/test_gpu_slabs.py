@@ -75,3 +75,96 @@ def test_four_slabs_converge_to_single_slab_solution():
     scale = max(np.max(np.abs(x)) for x in V1 + U1)
     err = max(np.max(np.abs(x - y)) for x, y in zip(V + U, list(V1) + list(U1)))
     assert err <= 1e-8 * scale
+
+
+# ---------------------------------------------------------------------------
+# the C++ slab set (smk_slabs_*: the V-cycle graph-captured, no Python per
+# colour pass) against the Python orchestrator, the hierarchy and the oracle
+# ---------------------------------------------------------------------------
+
+
+def c_setup(pb, slab_ids, n_slabs, n_levels, dtype=torch.float64):
+    from paper_1608_01102_b200 import nso
+    from paper_1608_01102_b200.fields import GridSpec
+    from paper_1608_01102_b200.slabs import build_c_solver
+    g = pb.g
+    spec = GridSpec(g.dim, g.res, g.h, g.boundary)
+    cfg = nso.StfasConfig(dt=pb.dt, K=pb.K, r=pb.r, n_levels=n_levels)
+    return spec, cfg, build_c_solver(spec, cfg, pb.v0, pb.vstar, slab_ids, n_slabs, pb.N, dtype)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_c_single_slab_equals_hierarchy_bitwise(dim):
+    """One C++ slab == the C++ hierarchy V-cycle (same kernels, halos = v0 and
+    the guide's own frames): bitwise, over two V-cycles + gauge + norms."""
+    from paper_1608_01102_b200 import nso
+    pb = make_problem(dim, n=16 if dim == 2 else 8, N=6, seed=211)
+    spec, cfg, (cs, st) = c_setup(pb, [0], 1, 3)
+    s = nso.SpacetimeState.zeros(spec, pb.N)
+    hier = nso.StfasHierarchy(spec, cfg, pb.N)
+    hier.set_guide(pb.v0, pb.vstar)
+    for _ in range(2):
+        cs.vcycle(st)
+        cs.gauge(st)
+        hier.vcycle(s)
+        hier.gauge_fix(s)
+    assert np.array_equal(flat_dev(st[0]), flat_dev(s))
+    assert cs.norms(st) == hier.residual_norms(s)
+    cs.close()
+    hier.close()
+
+
+@pytest.mark.parametrize("n_slabs", [2, 3, 4])
+def test_c_slabs_equal_python_orchestrator(n_slabs):
+    """S C++ slabs == the Python SlabSolver with the same S slabs (fused vs
+    unfused colour passes: same arithmetic), to rounding."""
+    pb = make_problem(3, n=8, N=7, seed=212)
+    _, _, (ps, pst) = setup(pb, list(range(n_slabs)), n_slabs, 2)
+    _, _, (cs, cst) = c_setup(pb, list(range(n_slabs)), n_slabs, 2)
+    for _ in range(2):
+        ps.vcycle(pst)
+        ps.gauge(pst)
+        cs.vcycle(cst)
+        cs.gauge(cst)
+    for a, b in zip(cst, pst):
+        x, y = flat_dev(a), flat_dev(b)
+        assert np.max(np.abs(x - y)) <= 1e-13 * np.max(np.abs(y))
+    ri_c, r2_c = cs.norms(cst)
+    ri_p, r2_p = ps.norms(pst)
+    assert abs(ri_c - ri_p) <= 1e-12 * ri_p and abs(r2_c - r2_p) <= 1e-12 * r2_p
+    cs.close()
+    ps.close()
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_c_two_slabs_match_oracle_slabs(dim):
+    n = 16 if dim == 2 else 8
+    pb = make_problem(dim, n=n, N=6, seed=202)
+    _, _, (cs, cst) = c_setup(pb, [0, 1], 2, 2)
+    osolver, ostates = build_oracle_solver(pb, 2, [0, 1], 2)
+    for _ in range(2):
+        cs.vcycle(cst)
+        cs.gauge(cst)
+        osolver.vcycle(ostates)
+        osolver.gauge(ostates)
+    for d, o in zip(cst, ostates):
+        a, b = flat_dev(d), flat_np(o)
+        assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
+    cs.close()
+
+
+def test_c_four_slabs_converge_to_single_slab_solution():
+    pb = make_problem(2, n=16, N=8, seed=203)
+    _, _, (one, s1) = c_setup(pb, [0], 1, 3)
+    one.solve(s1, eps=1e-10, cycle_budget=80)
+    _, _, (four, s4) = c_setup(pb, [0, 1, 2, 3], 4, 3)
+    h4 = four.solve(s4, eps=1e-10, cycle_budget=120)
+    assert h4[-1][1] <= 1e-10
+    V = [np.concatenate([st.numpy()[0][k] for st in s4]) for k in range(2)]
+    U = [np.concatenate([st.numpy()[2][k] for st in s4]) for k in range(2)]
+    V1, _, U1, _ = s1[0].numpy()
+    scale = max(np.max(np.abs(x)) for x in V1 + U1)
+    err = max(np.max(np.abs(x - y)) for x, y in zip(V + U, list(V1) + list(U1)))
+    assert err <= 1e-8 * scale
+    one.close()
+    four.close()
