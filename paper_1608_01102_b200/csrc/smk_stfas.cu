@@ -1675,6 +1675,14 @@ struct Nso : NsoBase {
     const int64_t per_pair = std::max((int64_t)Line<DIM>::SE * maxM, (int64_t)Line<DIM>::RS * rec_m);
     scratch = alloc((int64_t)N * per_pair);
     xout = alloc((int64_t)2 * N * B * maxM);
+    // SMK_POISON=1 (tests): the smoother's hand-off and delta buffers start
+    // as NaN, so a kernel reading an entry no kernel of the pass wrote shows
+    // up as a NaN in the result (initcheck stand-in; compute-sanitizer is not
+    // available on the GPU pool)
+    if (ok && getenv("SMK_POISON") && atoi(getenv("SMK_POISON"))) {
+      cudaMemset(scratch, 0xFF, (size_t)N * per_pair * sizeof(R));
+      cudaMemset(xout, 0xFF, (size_t)2 * N * B * maxM * sizeof(R));
+    }
     vswap.resize(lv.size());
     for (size_t l = 0; l < lv.size(); ++l) {
       for (int k = 0; k < 3; ++k)
