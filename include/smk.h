@@ -185,6 +185,10 @@ void smk_nso_destroy(smk_nso* h);
 int smk_nso_levels(const smk_nso* h);
 /* device bytes owned by the hierarchy (memtrack equivalent, memtrack.py:19-59) */
 int64_t smk_nso_device_bytes(const smk_nso* h);
+/* field-payload values owned by the hierarchy (coarse-level states, FAS rhs,
+ * residuals, guides; not the smoother's hand-off / delta scratch) --
+ * memtrack.py:1-9's accounting, for SPEC.md:529's memory bound */
+int64_t smk_nso_payload_values(const smk_nso* h);
 /* Bind the (device) v0 / vstar of the top level; restricts them down the
  * hierarchy.  Must be called before vcycle/solve and again when they change. */
 int smk_nso_set_guide(smk_nso* h, const void* const v0[], const void* const vstar[], void* stream);

@@ -100,6 +100,7 @@ SIGNATURES = {
     "smk_nso_profile_read_level": (I, [P, I, I, PD, ctypes.POINTER(ctypes.c_longlong),
                                        ctypes.POINTER(ctypes.c_longlong)]),
     "smk_nso_device_bytes": (I64, [P]),
+    "smk_nso_payload_values": (I64, [P]),
     "smk_nso_set_guide": (I, [P, P, P, P]),
     "smk_nso_set_K": (I, [P, D]),
     "smk_nso_vcycle": (I, [P, PS, P]),

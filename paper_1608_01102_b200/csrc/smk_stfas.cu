@@ -385,25 +385,19 @@ __device__ __forceinline__ double pivot_rcp(double x) { return 1.0 / x; }
 // is positive definite): on exit T[r][c] (c < r) = L[r][c], dinv = 1 / d.
 //
 // SingularBlock ("block pivot below 1e-12"), made scale-free:
-// the blocks are K' = [[D~, g], [g^T, 0]], so a faces pivot is compared with
-// tiny * s (s = the largest diagonal of D~) and the saddle pivot, which has
-// units of |g|^2 / D~, with tiny * sigma / s (sigma = |g|^2).  tiny = 1e-12
-// in both precisions: in fp32 it flags breakdown (zero / denormal / NaN
+// the blocks are K' = [[D~, g], [g^T, 0]] with D~ ~ (PM)^T PM + alpha I +
+// P / dt^2, so a faces pivot is compared with tf = 1e-12 (1/dt^2 + alpha)
+// and the saddle pivot (units |g|^2 / D~) with ts = 1e-12 sigma / (1/dt^2 +
+// alpha), sigma = |g|^2 -- per-cell constants, nothing on the elimination's
+// critical path.  In fp32 this flags breakdown (zero / denormal / NaN
 // pivots), in fp64 the SPEC's degenerate configurations too.
 template <class R, int B>
-__device__ __forceinline__ bool ldlt(R (&T)[B][B], R (&dinv)[B], R tiny) {
+__device__ __forceinline__ bool ldlt(R (&T)[B][B], R (&dinv)[B], R tf, R ts) {
   bool ok = true;
-  R smax = R(0), sig = R(0);
-#pragma unroll
-  for (int k = 0; k < B - 1; ++k) {
-    smax = fmax(smax, rabs(T[k][k]));
-    sig += T[B - 1][k] * T[B - 1][k];
-  }
 #pragma unroll
   for (int col = 0; col < B; ++col) {
     const R piv = T[col][col];
-    const R ref = col < B - 1 ? smax : sig / smax;
-    if (!(rabs(piv) > tiny * ref)) ok = false;
+    if (!(rabs(piv) > (col < B - 1 ? tf : ts))) ok = false;
     dinv[col] = pivot_rcp(piv);
     R l[B];
 #pragma unroll
@@ -685,6 +679,14 @@ struct LineCell {
 #pragma unroll
     for (int q = 0; q < NF; ++q) sigma += cg.gcol[q] * cg.gcol[q];
     isig = R(1) / sigma;
+    sig = sigma;
+  }
+  R sig;
+  // SingularBlock thresholds of the pairs with shift alpha (see ldlt)
+  __device__ __forceinline__ void piv_ref(R idt2, R alpha, R& tf, R& ts) const {
+    const R d = idt2 + alpha;
+    tf = R(1e-12) * d;
+    ts = R(1e-12) * sig / d;
   }
   // P x on the unknown faces (g is zero on walls)
   __device__ __forceinline__ void projP(R (&x)[NF]) const {
@@ -908,7 +910,9 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   // through Y = L^-1 [P M_{i+1}; 0]:  D~_{i+1} = D_{i+1} - Y^T diag(1/d) Y / dt^2,
   // and the back substitution needs W_i dv = K'^-1 [-P M_{i+1} dv / dt; 0],
   // so the pair hands off only D~_i and its rhs -- no explicit W.
-  const R tinyv = R(1e-12);   // relative SingularBlock threshold (ldlt / dense_solve)
+  const R tinyv = R(1e-12);   // relative SingularBlock threshold of dense_solve (the alpha = 0 pair)
+  R tf, ts;                    // ldlt thresholds of the alpha = K/r pairs
+  lc.piv_ref(idt2, cx.kr, tf, ts);
   // The dense block algebra below runs on lane pairs (columns 2h, 2h+1):
   // FFMA2 with a broadcast scalar in fp32, each lane rounded exactly like the
   // scalar FFMA of the same expression (same operand order, same summation
@@ -1039,7 +1043,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     build_rhs(cn, b);
     if (CMP && act) store_pair(i, b);
     saddle();
-    ok &= ldlt<R, B>(T, dinv, tinyv);
+    ok &= ldlt<R, B>(T, dinv, tf, ts);
     ldlt_solve<R, B>(T, dinv, b);
     if (!CMP && act) store_factors(i, dinv, b);
     P2 PM[NF][NH];
@@ -1093,7 +1097,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
     saddle();
     if (cx.t0 + i < cx.Ng - 1) {
       R dinv[B];
-      ok &= ldlt<R, B>(T, dinv, tinyv);
+      ok &= ldlt<R, B>(T, dinv, tf, ts);
       ldlt_solve<R, B>(T, dinv, b);
     } else {
       // alpha = 0: D~ is singular along M^-1 g; the saddle is not -> pivot
@@ -1162,7 +1166,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   const auto& cg = lc.cg;
   const Loc<DIM, PER, NX> L(ix, cg.c);
   const R idt = cx.idt;
-  const R tinyv = R(1e-12);   // relative SingularBlock threshold (ldlt / dense_solve)
+  const R tinyv = R(1e-12);   // relative SingularBlock threshold of dense_solve (the alpha = 0 pair)
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
   // inputs of step i: hand-off of pair i; u-rows of pair i+1 and the V
   // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
@@ -1273,7 +1277,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
       for (int a = 0; a < NF; ++a) T[NF][a] = cg.gcol[a];
       T[NF][NF] = R(0);
       if (i + 1 < N || cx.t0 + i < cx.Ng - 1) {
-        ldlt<R, B>(T, dinv, tinyv);
+        ldlt<R, B>(T, dinv, R(0), R(0));   // same factors as the forward; its flag is not re-raised
         ldlt_solve<R, B>(T, dinv, xb);
       } else {
         saddle_solve_pivot<R, B>(T, xb, tinyv);
@@ -1551,6 +1555,7 @@ struct NsoBase {
   virtual int profile(int enable) = 0;
   virtual int profile_read(int kind, int level, double* ms, long long* launches, long long* cells) = 0;
   virtual int64_t bytes() const = 0;
+  virtual int64_t payload() const = 0;
 };
 
 template <int DIM, bool PER, class R>
@@ -1599,11 +1604,16 @@ struct Nso : NsoBase {
     ++ev_used[kind];
   }
 
-  R* alloc(int64_t n) {
+  // field payload values owned by the hierarchy (memtrack.py:1-9 counts
+  // field containers, not solver scratch): every allocation except the
+  // smoother's hand-off and delta buffers
+  int64_t npayload = 0;
+  R* alloc(int64_t n, bool payload = true) {
     void* p = mem.get((size_t)n * sizeof(R));
     if (!p) ok = false;
     else cudaMemset(p, 0, (size_t)n * sizeof(R));
     nbytes += n * (int64_t)sizeof(R);
+    if (payload) npayload += n;
     return (R*)p;
   }
 
@@ -1673,8 +1683,8 @@ struct Nso : NsoBase {
     // fewer than fwd_mid cells): RS
     const int64_t rec_m = back_deep ? (maxM < fwd_mid ? maxM : fwd_mid) : 0;
     const int64_t per_pair = std::max((int64_t)Line<DIM>::SE * maxM, (int64_t)Line<DIM>::RS * rec_m);
-    scratch = alloc((int64_t)N * per_pair);
-    xout = alloc((int64_t)2 * N * B * maxM);
+    scratch = alloc((int64_t)N * per_pair, false);
+    xout = alloc((int64_t)2 * N * B * maxM, false);
     // SMK_POISON=1 (tests): the smoother's hand-off and delta buffers start
     // as NaN, so a kernel reading an entry no kernel of the pass wrote shows
     // up as a NaN in the result (initcheck stand-in; compute-sanitizer is not
@@ -1739,6 +1749,7 @@ struct Nso : NsoBase {
       }
   }
   int64_t bytes() const override { return nbytes; }
+  int64_t payload() const override { return npayload; }
 
   // slab halos for the next residual / colour pass (set by the level API)
   const void* halo_vprev[3] = {nullptr, nullptr, nullptr};
@@ -2888,6 +2899,7 @@ void smk_nso_destroy(smk_nso* h) {
 }
 
 int smk_nso_levels(const smk_nso* h) { return h ? h->impl->levels() : 0; }
+int64_t smk_nso_payload_values(const smk_nso* h) { return h ? h->impl->payload() : 0; }
 int smk_nso_n_colors(const smk_nso* h) { return h ? h->impl->ncolors() : 0; }
 
 int smk_nso_level_residual(smk_nso* h, int level, const smk_state* s, const void* const vprev[],

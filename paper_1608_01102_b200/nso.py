@@ -18,7 +18,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import _dev, _lib
+from . import _dev, _lib, memtrack
 from .errors import NonConvergence
 from .fields import GridSpec
 
@@ -71,6 +71,10 @@ class SpacetimeState:
     U: tuple
     P: torch.Tensor
 
+    def __post_init__(self):
+        for t in (*self.V, self.PB, *self.U, self.P):
+            memtrack.register(t)
+
     @classmethod
     def zeros(cls, spec, N, dtype=torch.float64):
         _dev.require_device()
@@ -118,6 +122,10 @@ class SpacetimeResidual:
     R2: torch.Tensor
     R3: tuple
     R4: torch.Tensor
+
+    def __post_init__(self):
+        for t in (*self.R1, self.R2, *self.R3, self.R4):
+            memtrack.register(t)
 
     @classmethod
     def zeros(cls, spec, N, dtype=torch.float64):
@@ -230,6 +238,7 @@ class StfasHierarchy:
             _lib.check(_lib.SMK_ERR_CUDA if "alloc" in _lib.last_error() else _lib.SMK_ERR_ARG, "nso_create")
         self._h = h
         self._guide = None
+        self._payload = memtrack.OwnedPayload(L.smk_nso_payload_values(h))
 
     @property
     def levels(self):
@@ -243,6 +252,7 @@ class StfasHierarchy:
         if getattr(self, "_h", None):
             self._L.smk_nso_destroy(self._h)
             self._h = None
+            self._payload = None
 
     def __del__(self):
         try:
