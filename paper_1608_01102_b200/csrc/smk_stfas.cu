@@ -13,6 +13,7 @@
 // (snapshot reads, writes go to a delta buffer), then the colour's unknowns
 // take x += omega * dx.  Same-colour cells own disjoint unknowns, so the
 // apply pass is race-free and the sweep is bitwise deterministic.
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +30,10 @@
 #include "smk_internal.cuh"
 
 namespace smk {
+
+#ifndef SMK_HANDOFF_BLOCKED
+#define SMK_HANDOFF_BLOCKED 1
+#endif
 
 template <class R>
 struct StP {
@@ -76,7 +81,10 @@ struct KktCtx {
 
   // K-term / u_{i+1} present for local pair i (global i < Ng-1)
   __device__ __forceinline__ bool inner(int i) const { return t0 + i < Ng - 1; }
-  __device__ __forceinline__ Face3<R> u_next(int i) const { return i < N - 1 ? frame_of(U, i + 1, nf) : un; }
+  // frame fr of a face stack.  (32-bit frame offsets without the null
+  // checks were measured slower: cfg5 V-cycle 145 -> 169 ms.)
+  __device__ __forceinline__ Face3<R> frame(const Face3<R>& base, int fr) const { return frame_of(base, fr, nf); }
+  __device__ __forceinline__ Face3<R> u_next(int i) const { return i < N - 1 ? frame(U, i + 1) : un; }
 };
 
 // ---------------------------------------------------------------------------
@@ -165,7 +173,7 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
   const R* PBi = cx.PB + (int64_t)i * cx.nc;
   const bool inner = cx.inner(i);
   const Face3<R> Un = inner ? cx.u_next(i) : Face3<R>{};
-  const Face3<R> Vs = inner ? frame_of(cx.vs, i + 1, cx.nf) : Face3<R>{};
+  const Face3<R> Vs = inner ? cx.frame(cx.vs, i + 1) : Face3<R>{};
   // gather every scalar input first, so all of the pair's loads are in
   // flight together (one memory latency per pair, not one per face)
   RowIn<DIM, R> g;
@@ -232,9 +240,9 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
       wall[2 * k + 1] = !PER && c[k] == ix.n(k) - 1;
     }
     R VC[DIM][NB], UC[DIM][NB];
-    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
-    load_nbr<DIM, PER, R>(ix, L, frame_of(cx.U, i, cx.nf), UC);
-    const Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
+    load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i), VC);
+    load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.U, i), UC);
+    const Face3<R> Vp = i == 0 ? cx.v0 : cx.frame(cx.V, i - 1);
     R vp[NF];
 #pragma unroll
     for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
@@ -622,6 +630,17 @@ struct Line {
   static constexpr int T0 = 0, B0 = NT, Y0 = NL + 2 * B;
   static constexpr int L0 = 0, D0 = NL, Z0 = NL + B;
   static constexpr int SE = NL + 3 * B;
+  // [i][e][m] formats are stored block-interleaved, [i][m / HB][e][HB]: a
+  // pair's entries of HB consecutive colour cells are one contiguous
+  // SE x HB tile, so a thread addresses entry e of pair i as
+  // base_i + e * HB (an immediate offset on one per-pair pointer) instead of
+  // a 64-bit (i SE + e) M + m product per access; every warp access is still
+  // one coalesced 128-byte row.
+  static constexpr int HB = SMK_HANDOFF_BLOCKED ? 64 : 1;
+  __host__ __device__ static int64_t pair_stride(int64_t M) { return ((M + HB - 1) / HB) * SE * HB; }
+  __host__ __device__ static int64_t cell_base(int64_t m) { return (m / HB) * SE * HB + (m % HB); }
+  // entry stride of the tile (HB = 1: the plain [i][e][m] layout, stride M)
+  __host__ __device__ static int64_t entry_stride(int64_t M) { return HB > 1 ? HB : M; }
   // record hand-off (shape-2 colours with the cp.async-ring backward): RS
   // values per (pair, cell) -- M_i (row-major, written by the pair's
   // producer), yu_i (padded to 8), then the consumer's L, 1/d and z -- in
@@ -811,7 +830,13 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
   const auto& cg = lc.cg;
   const R c0 = cx.c0;
   const R idt = cx.idt;
+#if SMK_HANDOFF_BLOCKED
+  R* const hbase = scratch + LN::cell_base(act ? m : 0);
+  const int64_t hstride = LN::pair_stride(M);
+  auto sc = [&](int i, int e) -> R* { return hbase + (int64_t)i * hstride + e * LN::HB; };
+#else
   auto sc = [&](int i, int e) -> R* { return scratch + ((int64_t)i * LN::SE + e) * M + m; };
+#endif
   auto slot = [&](int i, int e) -> R* { return ring + ((i % S) * NE + e) * TM + lane; };
   const R idt2 = idt * idt;
   R gs[NF];   // g * idt^2 / sigma: P idt^2 = idt^2 I - g gs^T on the unknown faces
@@ -830,14 +855,14 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
       if (i >= S) nb_sync(1 + S + i % S, NT);   // EMPTY: the consumers released pair i - S
       if (act) {
         if (P > 1) {
-          const Face3<R> Vp = i == 0 ? cx.v0 : frame_of(cx.V, i - 1, cx.nf);
+          const Face3<R> Vp = i == 0 ? cx.v0 : cx.frame(cx.V, i - 1);
 #pragma unroll
           for (int q = 0; q < NF; ++q) vp[q] = Vp.c[q >> 1][L.of[q]];
         }
         R VC[DIM][NB], UC[DIM][NB];
         R yu[B], yv[B];
-        load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i, cx.nf), VC);
-        load_nbr<DIM, PER, R>(ix, L, frame_of(cx.U, i, cx.nf), UC);
+        load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i), VC);
+        load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.U, i), UC);
         pair_rows<DIM, PER, R, true, false, HR>(cx, L, cg.wall, i, VC, UC, vp, rhs, yu, yv);
 #pragma unroll
         for (int q = 0; q < B; ++q) {
@@ -1167,7 +1192,13 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   const Loc<DIM, PER, NX> L(ix, cg.c);
   const R idt = cx.idt;
   const R tinyv = R(1e-12);   // relative SingularBlock threshold of dense_solve (the alpha = 0 pair)
+#if SMK_HANDOFF_BLOCKED
+  const R* const hbase = scratch + LN::cell_base(m);
+  const int64_t hstride = LN::pair_stride(M);
+  auto sc = [&](int i, int e) -> R { return __ldg(hbase + (int64_t)i * hstride + e * LN::HB); };
+#else
   auto sc = [&](int i, int e) -> R { return __ldg(scratch + ((int64_t)i * LN::SE + e) * M + m); };
+#endif
   // inputs of step i: hand-off of pair i; u-rows of pair i+1 and the V
   // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
   auto fetch = [&](int i, BackIn<DIM, R, CMP>& in) {
@@ -1186,7 +1217,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
     if (i + 1 < N) {
 #pragma unroll
       for (int q = 0; q < B; ++q) in.yu[q] = sc(i + 1, LN::Y0 + q);
-      load_nbr<DIM, PER, R>(ix, L, frame_of(cx.V, i + 1, cx.nf), in.VC);
+      load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i + 1), in.VC);
     }
     if constexpr (FUSE) {
       if (i + 1 < N) {
@@ -1682,7 +1713,7 @@ struct Nso : NsoBase {
     // [i][e][m] formats: SE values per pair; record format (shape-2 colours,
     // fewer than fwd_mid cells): RS
     const int64_t rec_m = back_deep ? (maxM < fwd_mid ? maxM : fwd_mid) : 0;
-    const int64_t per_pair = std::max((int64_t)Line<DIM>::SE * maxM, (int64_t)Line<DIM>::RS * rec_m);
+    const int64_t per_pair = std::max(Line<DIM>::pair_stride(maxM), (int64_t)Line<DIM>::RS * rec_m);
     scratch = alloc((int64_t)N * per_pair, false);
     xout = alloc((int64_t)2 * N * B * maxM, false);
     // SMK_POISON=1 (tests): the smoother's hand-off and delta buffers start
