@@ -187,10 +187,7 @@ def cmd_optimize(args, cfg=None):
 
 
 def _run_lbfgs(cfg, spec, rho0, kf, out):
-    try:
-        from . import lbfgs
-    except ImportError:
-        raise SmokeCtrlError("the LBFGS baseline (SPEC.md:428-472) is not part of this build") from None
+    from . import lbfgs
     t0 = time.perf_counter()
     res = lbfgs.minimize(spec, rho0, kf, cfg.r, cfg.timestep(), dtype=_dtype(cfg))
     n = res.rho.shape[0] - 1

@@ -628,6 +628,9 @@ struct Line {
   //   factored (small, latency-bound colours): L (strict lower), 1/d, z, yu
   static constexpr int NT = NF * (NF + 1) / 2, NL = B * (B - 1) / 2;
   static constexpr int T0 = 0, B0 = NT, Y0 = NL + 2 * B;
+  // compact keeps its yu right after b, so a pair's compact entries are the
+  // contiguous rows [0, NCMP) of its tile (one bulk copy per block, k_scgs_back)
+  static constexpr int Y0C = NT + B, NCMP = NT + 2 * B;
   static constexpr int L0 = 0, D0 = NL, Z0 = NL + B;
   static constexpr int SE = NL + 3 * B;
   // [i][e][m] formats are stored block-interleaved, [i][m / HB][e][HB]: a
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
         for (int q = 0; q < B; ++q) {
           yu[q] = -yu[q];
           yv[q] = -yv[q];
-          if constexpr (!REC) *sc(i, LN::Y0 + q) = yu[q];
+          if constexpr (!REC) *sc(i, (CMP ? LN::Y0C : LN::Y0) + q) = yu[q];
         }
         if constexpr (REC) {
           // M_i and yu_i for the backward's step of pair i - 1 (M from the
@@ -1153,6 +1156,33 @@ __global__ void __launch_bounds__((P + 1) * TM, fwd_min_blocks(TM, P, sizeof(R))
 // PIPE (small colours, latency-bound): the loads of step i-1 (its hand-off,
 // u-rows and V stencil) are issued before step i computes, so one memory
 // latency overlaps one step instead of adding to it.
+
+// ---- mbarrier + 1D bulk async copy (TMA engine) helpers -------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int DIM, class R, bool CMP>
 struct BackIn {
   static constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
@@ -1176,17 +1206,55 @@ struct BackIn {
 #ifndef SMK_BACK_MINB
 #define SMK_BACK_MINB 1
 #endif
-template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP, bool FUSE>
+// TMA (compact + fused, 128-thread CTAs = two 64-cell hand-off blocks, the
+// host launches it only when the colour is a multiple of 128 cells): the
+// compact entries of pair i for the CTA's two blocks (2 x 35 x 64 values,
+// contiguous per block) arrive by two 1D bulk async copies issued one step
+// ahead by thread 0 into a 2-stage shared-memory ring, completion on an
+// mbarrier per stage; the thread reads its t / b / yu from shared memory, so
+// the 42 hand-off loads per step and their address math leave the serial
+// chain.  One __syncthreads per step frees the stage the next copy targets.
+template <int DIM, class R>
+__host__ __device__ constexpr size_t back_tma_smem() {
+  return (size_t)2 * 2 * Line<DIM>::NCMP * Line<DIM>::HB * sizeof(R);
+}
+template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP, bool FUSE, bool TMA = false>
 __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
                                                    int m1, int m2, R omega, const R* __restrict__ scratch,
                                                    R* __restrict__ xout, StP<R> so) {
   using LN = Line<DIM>;
   constexpr int NF = LN::NF, B = LN::B, NTT = CMP ? LN::NT : LN::NL;
+  static_assert(!TMA || (CMP && FUSE && !PIPE && SMK_HANDOFF_BLOCKED), "TMA: compact fused blocked hand-off only");
   const auto& ix = cx.ix;
   const int N = cx.N;
   const int64_t M = (int64_t)m0 * m1 * m2;
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= M) return;
+  if (m >= M) return;   // TMA: never taken (M % 128 == 0)
+  extern __shared__ __align__(128) unsigned char tsm_raw[];
+  __shared__ __align__(8) uint64_t tbar[2];
+  constexpr int NC = LN::NCMP, HB = LN::HB;
+  R* const tring = reinterpret_cast<R*>(tsm_raw);   // [stage][block][NC][HB]
+  const int tblk = threadIdx.x / HB, tl = threadIdx.x % HB;
+  auto tmem = [&](int i, int e) -> R { return tring[(((i & 1) * 2 + tblk) * NC + e) * HB + tl]; };
+  auto tissue = [&](int i) {   // thread 0: pair i's compact entries of both blocks
+    if (threadIdx.x != 0 || i < 0) return;
+    const uint32_t bytes = NC * HB * sizeof(R);
+    uint64_t* bar = &tbar[i & 1];
+    mbar_expect_tx(bar, 2 * bytes);
+    const int64_t b0 = (int64_t)blockIdx.x * 2;
+    for (int j = 0; j < 2; ++j)
+      bulk_g2s(tring + ((i & 1) * 2 + j) * NC * HB, scratch + (int64_t)i * LN::pair_stride(M) + (b0 + j) * LN::SE * HB,
+               bytes, bar);
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar[0], 1);
+      mbar_init(&tbar[1], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    tissue(N - 1);
+  }
   const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
   const auto& cg = lc.cg;
   const Loc<DIM, PER, NX> L(ix, cg.c);
@@ -1202,6 +1270,33 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   // inputs of step i: hand-off of pair i; u-rows of pair i+1 and the V
   // stencil of frame i+1 (i = -1: only the u-rows / stencil of pair 0)
   auto fetch = [&](int i, BackIn<DIM, R, CMP>& in) {
+    if constexpr (TMA) {
+      // yu_{i+1} from pair i+1's stage (landed last step), then free that
+      // stage and launch pair i-1 into it; the V stencil and the targets by
+      // plain loads; pair i's t / b once its copy has landed
+      if (i + 1 < N) {
+#pragma unroll
+        for (int q = 0; q < B; ++q) in.yu[q] = tmem(i + 1, LN::Y0C + q);
+      }
+      __syncthreads();
+      tissue(i - 1);
+      if (i + 1 < N) load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i + 1), in.VC);
+      if (i + 1 < N) {
+#pragma unroll
+        for (int q = 0; q < NF; ++q)
+          in.uo[q] = cg.wall[q] ? R(0) : so.U[q >> 1][(int64_t)(i + 1) * cx.nf[q >> 1] + L.of[q]];
+        in.po = so.P[(int64_t)(i + 1) * cx.nc + L.co];
+      }
+      if (i >= 0) {
+        in.pbo = so.PB[(int64_t)i * cx.nc + L.co];
+        mbar_wait(&tbar[i & 1], (uint32_t)(((N - 1 - i) >> 1) & 1));
+#pragma unroll
+        for (int e = 0; e < NTT; ++e) in.t[e] = tmem(i, LN::T0 + e);
+#pragma unroll
+        for (int r = 0; r < B; ++r) in.b[r] = tmem(i, LN::B0 + r);
+      }
+      return;
+    }
     if (i >= 0) {
       if (CMP || i + 1 < N) {
 #pragma unroll
@@ -1216,7 +1311,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
     }
     if (i + 1 < N) {
 #pragma unroll
-      for (int q = 0; q < B; ++q) in.yu[q] = sc(i + 1, LN::Y0 + q);
+      for (int q = 0; q < B; ++q) in.yu[q] = sc(i + 1, (CMP ? LN::Y0C : LN::Y0) + q);
       load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i + 1), in.VC);
     }
     if constexpr (FUSE) {
@@ -1889,6 +1984,9 @@ struct Nso : NsoBase {
   // buffer, no apply kernel, V ping-pongs through vswap[l]); the record
   // backward of the small colours keeps deltas + apply.  SMK_NO_FUSE=1 off.
   bool fuse_env = getenv("SMK_NO_FUSE") == nullptr || atoi(getenv("SMK_NO_FUSE")) == 0;
+  // the compact fused backward stages its hand-off with bulk async copies
+  // (k_scgs_back<..., TMA>); SMK_BACK_TMA=0 off
+  bool back_tma = getenv("SMK_BACK_TMA") == nullptr || atoi(getenv("SMK_BACK_TMA")) != 0;
   bool fusable(int l) const {
     if (!prm.red_black || !fuse_env) return false;
     int o[3], mm[3];
@@ -1992,6 +2090,20 @@ struct Nso : NsoBase {
       auto back = [&](auto pipe, auto nxc, auto cmpc) {
         constexpr bool PIPEv = decltype(pipe)::value, CMPv = decltype(cmpc)::value;
         constexpr int NXv = decltype(nxc)::value;
+        if constexpr (CMPv && !PIPEv && SMK_HANDOFF_BLOCKED) {
+          if (fuse_out && back_tma && tpb == 128 && M % 128 == 0) {
+            auto kern = k_scgs_back<DIM, PER, R, false, NXv, true, true, true>;
+            const size_t shm = back_tma_smem<DIM, R>();
+            static bool attr = false;
+            if (!attr) {
+              cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+              attr = true;
+            }
+            kern<<<gb, tpb, shm, st>>>(c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout,
+                                       so);
+            return;
+          }
+        }
         if (fuse_out)
           k_scgs_back<DIM, PER, R, PIPEv, NXv, CMPv, true><<<gb, tpb, 0, st>>>(
               c, o[0], o[1], o[2], mod, mm[0], mm[1], mm[2], (R)prm.omega, scratch, xout, so);

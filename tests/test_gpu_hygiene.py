@@ -63,8 +63,10 @@ def test_shapes_deterministic_and_poison_clean(nso, monkeypatch, shape, dtype):
     monkeypatch.setenv("SMK_BACK_FLAT", bf)
     monkeypatch.setenv("SMK_BACK_DEEP", deep)
     monkeypatch.setenv("SMK_NO_GRAPH", "1")
-    # 3D 32^3 x 6: 16,384 colour cells, many CTAs per SM on every shape
-    pb = make_problem(3, n=32, N=6, seed=61)
+    # 3D 32^3 x 6: 16,384 colour cells, many CTAs per SM on every shape;
+    # tm64p1-cmp also at 48^3 (55,296 colour cells: the TMA-staged fused
+    # backward, which needs 128-cell CTAs and a multiple of 128 cells)
+    pb = make_problem(3, n=48 if name == "tm64p1-cmp" else 32, N=6, seed=61)
     ref, ri = run_vcycle(nso, pb, dtype)
     assert np.all(np.isfinite(ref))
     for _ in range(2):
