@@ -1190,8 +1190,14 @@ struct BackIn {
   R t[CMP ? NF * (NF + 1) / 2 : B * (B - 1) / 2], b[B], d[CMP ? 1 : B], yu[B];
   R VC[DIM][NB];
   // FUSE: the in-place targets of the step (U, P of pair i+1, PBAR of pair i),
-  // loaded with the step's other inputs so no extra latency joins the chain
+  // loaded with the step's other inputs so no extra latency joins the chain,
+  // and the frame pointers of their stores (one 64-bit product per array and
+  // step instead of one per access)
   R uo[NF], po, pbo;
+  R* fu[DIM];
+  R* fv[DIM];
+  R* fp;
+  R* fpb;
 };
 
 // FUSE (red-black, where every face of the grid has exactly one cell of the
@@ -1235,7 +1241,8 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   constexpr int NC = LN::NCMP, HB = LN::HB;
   R* const tring = reinterpret_cast<R*>(tsm_raw);   // [stage][block][NC][HB]
   const int tblk = threadIdx.x / HB, tl = threadIdx.x % HB;
-  auto tmem = [&](int i, int e) -> R { return tring[(((i & 1) * 2 + tblk) * NC + e) * HB + tl]; };
+  const R* const tr0 = tring + tblk * NC * HB + tl;   // stage 0 of this thread's block; stage 1 at + 2 NC HB
+  auto tmem = [&](int i, int e) -> R { return tr0[(i & 1) * 2 * NC * HB + e * HB]; };
   auto tissue = [&](int i) {   // thread 0: pair i's compact entries of both blocks
     if (threadIdx.x != 0 || i < 0) return;
     const uint32_t bytes = NC * HB * sizeof(R);
@@ -1283,12 +1290,18 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
       if (i + 1 < N) load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i + 1), in.VC);
       if (i + 1 < N) {
 #pragma unroll
-        for (int q = 0; q < NF; ++q)
-          in.uo[q] = cg.wall[q] ? R(0) : so.U[q >> 1][(int64_t)(i + 1) * cx.nf[q >> 1] + L.of[q]];
-        in.po = so.P[(int64_t)(i + 1) * cx.nc + L.co];
+        for (int k = 0; k < DIM; ++k) {
+          in.fu[k] = so.U[k] + (int64_t)(i + 1) * cx.nf[k];
+          in.fv[k] = so.V[k] + (int64_t)(i + 1) * cx.nf[k];
+        }
+        in.fp = so.P + (int64_t)(i + 1) * cx.nc;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) in.uo[q] = cg.wall[q] ? R(0) : in.fu[q >> 1][L.of[q]];
+        in.po = in.fp[L.co];
       }
       if (i >= 0) {
-        in.pbo = so.PB[(int64_t)i * cx.nc + L.co];
+        in.fpb = so.PB + (int64_t)i * cx.nc;
+        in.pbo = in.fpb[L.co];
         mbar_wait(&tbar[i & 1], (uint32_t)(((N - 1 - i) >> 1) & 1));
 #pragma unroll
         for (int e = 0; e < NTT; ++e) in.t[e] = tmem(i, LN::T0 + e);
@@ -1317,11 +1330,19 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
     if constexpr (FUSE) {
       if (i + 1 < N) {
 #pragma unroll
-        for (int q = 0; q < NF; ++q)
-          in.uo[q] = cg.wall[q] ? R(0) : so.U[q >> 1][(int64_t)(i + 1) * cx.nf[q >> 1] + L.of[q]];
-        in.po = so.P[(int64_t)(i + 1) * cx.nc + L.co];
+        for (int k = 0; k < DIM; ++k) {
+          in.fu[k] = so.U[k] + (int64_t)(i + 1) * cx.nf[k];
+          in.fv[k] = so.V[k] + (int64_t)(i + 1) * cx.nf[k];
+        }
+        in.fp = so.P + (int64_t)(i + 1) * cx.nc;
+#pragma unroll
+        for (int q = 0; q < NF; ++q) in.uo[q] = cg.wall[q] ? R(0) : in.fu[q >> 1][L.of[q]];
+        in.po = in.fp[L.co];
       }
-      if (i >= 0) in.pbo = so.PB[(int64_t)i * cx.nc + L.co];
+      if (i >= 0) {
+        in.fpb = so.PB + (int64_t)i * cx.nc;
+        in.pbo = in.fpb[L.co];
+      }
     }
   };
   // t = M dv from a V stencil
@@ -1351,9 +1372,8 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
     if constexpr (FUSE) {
 #pragma unroll
       for (int q = 0; q < NF; ++q)
-        if (!cg.wall[q])
-          so.U[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = in.uo[q] + omega * (cg.gcol[q] * dp - a[q]);
-      so.P[(int64_t)ip * cx.nc + L.co] = in.po + omega * dp;
+        if (!cg.wall[q]) in.fu[q >> 1][L.of[q]] = in.uo[q] + omega * (cg.gcol[q] * dp - a[q]);
+      in.fp[L.co] = in.po + omega * dp;
     } else {
       R* xo = xout + (int64_t)(2 * ip) * B * M + m;
 #pragma unroll
@@ -1366,7 +1386,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   auto v_store = [&](int ip, const BackIn<DIM, R, CMP>& in, const R (&dv)[NF]) {
 #pragma unroll
     for (int q = 0; q < NF; ++q)
-      if (!cg.wall[q]) so.V[q >> 1][(int64_t)ip * cx.nf[q >> 1] + L.of[q]] = in.VC[q >> 1][(q & 1) + 1] + omega * dv[q];
+      if (!cg.wall[q]) in.fv[q >> 1][L.of[q]] = in.VC[q >> 1][(q & 1) + 1] + omega * dv[q];
   };
   R xn[NF];   // dv of pair i+1
   R t[NF];    // M_{i+1} dv_{i+1}
@@ -1430,7 +1450,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
       for (int r = 0; r < B; ++r) xb[r] -= w[r];
     }
     if constexpr (FUSE) {
-      so.PB[(int64_t)i * cx.nc + L.co] = cur.pbo + omega * xb[NF];
+      cur.fpb[L.co] = cur.pbo + omega * xb[NF];
     } else {
       R* xo = xout + (int64_t)(2 * i + 1) * B * M + m;
 #pragma unroll
