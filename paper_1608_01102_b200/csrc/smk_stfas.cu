@@ -35,6 +35,7 @@ namespace smk {
 #define SMK_HANDOFF_BLOCKED 1
 #endif
 
+
 template <class R>
 struct StP {
   R* V[3];
@@ -85,6 +86,7 @@ struct KktCtx {
   // checks were measured slower: cfg5 V-cycle 145 -> 169 ms.)
   __device__ __forceinline__ Face3<R> frame(const Face3<R>& base, int fr) const { return frame_of(base, fr, nf); }
   __device__ __forceinline__ Face3<R> u_next(int i) const { return i < N - 1 ? frame(U, i + 1) : un; }
+
 };
 
 // ---------------------------------------------------------------------------
@@ -798,8 +800,13 @@ __host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P ==
 // (group p builds pairs i = p mod P, so the coarse levels -- few cells, long
 // time lines -- get P-fold producer parallelism), one consumer group.
 // resident CTAs per SM the register budget is sized for
+#ifndef SMK_FWD_MINB
+#define SMK_FWD_MINB 4
+#endif
 __host__ __device__ constexpr int fwd_min_blocks_f32(int TM, int P) {
-  return P == 1 ? 512 / (2 * TM) : (P == 2 ? 5 : 2);   // 128 registers on P <= 2 (more CTAs spill: measured slower)
+  // 128 registers on P <= 2 (more CTAs spill: measured slower); TM 64 / P 1
+  // at SMK_FWD_MINB CTAs per SM (tuning builds)
+  return P == 1 ? (TM == 64 ? SMK_FWD_MINB : 512 / (2 * TM)) : (P == 2 ? 5 : 2);
 }
 __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
   return esz == 8 ? (fwd_min_blocks_f32(TM, P) / 2 > 0 ? fwd_min_blocks_f32(TM, P) / 2 : 1) : fwd_min_blocks_f32(TM, P);
