@@ -239,32 +239,42 @@ def time_to_solution(nso, spec, w, v0, vstar, levels, budget):
     return out
 
 
+E2E_LANES = 3
+
+
 def e2e_pipelined(args, spec, cfg, w, v0, vstar, state, hier, h_in, out_h):
     """End-to-end throughput of a stream of independent solve calls with host
     buffers: each call uploads its inputs (guide + state) from pinned memory,
     runs set_guide + one V-cycle + gauge, and downloads the updated state.
-    Two buffer lanes (state, guide, hierarchy each) let call k+1's upload and
-    call k-1's download (copy engines, both PCIe directions) overlap call k's
-    V-cycle; every call still moves all of its bytes inside the timed region
-    (first upload start -> last download end, device events)."""
+    E2E_LANES buffer lanes (state, guide, hierarchy each) let call k+1's upload
+    and call k-1's download (copy engines, both PCIe directions at once) overlap
+    call k's V-cycle.  A lane is busy from its upload start to its download end
+    (upload + solve + download), so two lanes bound a call at half that sum;
+    three leave the period at the slowest of the three legs.  Every call still
+    moves all of its bytes inside the timed region (first upload start -> last
+    download end, device events)."""
     import torch
     from paper_1608_01102_b200 import nso
+    nl = E2E_LANES
     lanes = [(state, list(vstar), hier)]
-    st1 = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
-    vs1 = [torch.empty_like(c) for c in vstar]
-    for d, s_ in zip(vs1, vstar):
-        d.copy_(s_)
-    h1 = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
-    lanes.append((st1, vs1, h1))
-    outs = [out_h, [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out_h]]
+    extra = []
+    for _ in range(nl - 1):
+        st1 = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
+        vs1 = [torch.empty_like(c) for c in vstar]
+        for d, s_ in zip(vs1, vstar):
+            d.copy_(s_)
+        h1 = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
+        lanes.append((st1, vs1, h1))
+        extra.append(h1)
+    outs = [out_h] + [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in out_h] for _ in range(nl - 1)]
     sH, sC, sD = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
     arrays = lambda st: [*st.V, st.PB, *st.U, st.P]
 
     def call(k, done):
-        st, vs, hr = lanes[k % 2]
+        st, vs, hr = lanes[k % nl]
         d_in = list(vs) + arrays(st)
-        if done[k % 2] is not None:
-            sH.wait_event(done[k % 2])
+        if done[k % nl] is not None:
+            sH.wait_event(done[k % nl])
         with torch.cuda.stream(sH):
             for d, h in zip(d_in, h_in):
                 d.copy_(h, non_blocking=True)
@@ -279,29 +289,30 @@ def e2e_pipelined(args, spec, cfg, w, v0, vstar, state, hier, h_in, out_h):
             ec.record(sC)
         sD.wait_event(ec)
         with torch.cuda.stream(sD):
-            for h, d in zip(outs[k % 2], arrays(st)):
+            for h, d in zip(outs[k % nl], arrays(st)):
                 h.copy_(d, non_blocking=True)
             ed = torch.cuda.Event()
             ed.record(sD)
-        done[k % 2] = ed
+        done[k % nl] = ed
 
-    # untimed: one call per lane (graph capture of lane 1's V-cycle)
-    done = [None, None]
-    for k in range(2):
+    # untimed: one call per lane (graph capture of each lane's V-cycle)
+    done = [None] * nl
+    for k in range(nl):
         call(k, done)
     torch.cuda.synchronize()
-    reps = max(4, args.steps)
-    done = [None, None]
+    reps = max(4 * nl, args.steps)   # a stream of calls: fill + drain amortised over 12
+    done = [None] * nl
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(sH)
     for k in range(reps):
         call(k, done)
-    sD.wait_event(done[(reps - 1) % 2])
+    sD.wait_event(done[(reps - 1) % nl])
     e1.record(sD)
     e1.synchronize()
     torch.cuda.synchronize()
-    h1.close()
+    for h1 in extra:
+        h1.close()
     return e0.elapsed_time(e1) / reps, reps
 
 
@@ -502,7 +513,7 @@ def main():
             h2d, d2h = hb[0].item(), hb[1].item()
         e2e = {"value": w.cell_timesteps / (e_ms / 1000.0), "unit": "cell-updates/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms,
-               "calls": reps, "mode": ("pipelined: 2 buffer lanes, H2D / solve / D2H on three streams, "
+               "calls": reps, "mode": (f"pipelined: {E2E_LANES} buffer lanes, H2D / solve / D2H on three streams, "
                                        "calls k+1's upload and k-1's download overlap call k's V-cycle")
                if pipelined else "serial"}
 
