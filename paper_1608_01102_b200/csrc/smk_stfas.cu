@@ -803,10 +803,13 @@ __host__ __device__ constexpr int ring_stages(int P) { return P == 1 ? 3 : (P ==
 #ifndef SMK_FWD_MINB
 #define SMK_FWD_MINB 4
 #endif
+#ifndef SMK_FWD_MINB_64X2
+#define SMK_FWD_MINB_64X2 2
+#endif
 __host__ __device__ constexpr int fwd_min_blocks_f32(int TM, int P) {
   // 128 registers on P <= 2 (more CTAs spill: measured slower); TM 64 / P 1
   // at SMK_FWD_MINB CTAs per SM (tuning builds)
-  return P == 1 ? (TM == 64 ? SMK_FWD_MINB : 512 / (2 * TM)) : (P == 2 ? 5 : 2);
+  return P == 1 ? (TM == 64 ? SMK_FWD_MINB : 512 / (2 * TM)) : (P == 2 ? (TM == 64 ? SMK_FWD_MINB_64X2 : 5) : 2);
 }
 __host__ __device__ constexpr int fwd_min_blocks(int TM, int P, int esz) {
   return esz == 8 ? (fwd_min_blocks_f32(TM, P) / 2 > 0 ? fwd_min_blocks_f32(TM, P) / 2 : 1) : fwd_min_blocks_f32(TM, P);
@@ -1227,9 +1230,17 @@ struct BackIn {
 // mbarrier per stage; the thread reads its t / b / yu from shared memory, so
 // the 42 hand-off loads per step and their address math leave the serial
 // chain.  One __syncthreads per step frees the stage the next copy targets.
+// ring depth of the TMA-staged hand-off: the copy of pair i - (NS - 1) is
+// issued at step i, so NS - 1 pairs (2 x 8.96 KB each in fp32) are in flight
+// per CTA while a step computes
+#ifndef SMK_BACK_STAGES
+#define SMK_BACK_STAGES 3
+#endif
+template <class R>
+__host__ __device__ constexpr int back_tma_stages() { return sizeof(R) == 4 ? SMK_BACK_STAGES : 2; }
 template <int DIM, class R>
 __host__ __device__ constexpr size_t back_tma_smem() {
-  return (size_t)2 * 2 * Line<DIM>::NCMP * Line<DIM>::HB * sizeof(R);
+  return (size_t)back_tma_stages<R>() * 2 * Line<DIM>::NCMP * Line<DIM>::HB * sizeof(R);
 }
 template <int DIM, bool PER, class R, bool PIPE, int NX, bool CMP, bool FUSE, bool TMA = false>
 __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktCtx<DIM, PER, R> cx, int o0, int o1, int o2, int mod, int m0,
@@ -1244,30 +1255,33 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
   const int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;   // TMA: never taken (M % 128 == 0)
   extern __shared__ __align__(128) unsigned char tsm_raw[];
-  __shared__ __align__(8) uint64_t tbar[2];
+  constexpr int NS = back_tma_stages<R>();
+  __shared__ __align__(8) uint64_t tbar[NS];
   constexpr int NC = LN::NCMP, HB = LN::HB;
   R* const tring = reinterpret_cast<R*>(tsm_raw);   // [stage][block][NC][HB]
   const int tblk = threadIdx.x / HB, tl = threadIdx.x % HB;
-  const R* const tr0 = tring + tblk * NC * HB + tl;   // stage 0 of this thread's block; stage 1 at + 2 NC HB
-  auto tmem = [&](int i, int e) -> R { return tr0[(i & 1) * 2 * NC * HB + e * HB]; };
+  const R* const tr0 = tring + tblk * NC * HB + tl;   // stage 0 of this thread's block; stage s at + 2 s NC HB
+  // pair i lives in stage (N - 1 - i) % NS, in the ((N - 1 - i) / NS)-th use of its barrier
+  auto tstage = [&](int i) -> int { return (N - 1 - i) % NS; };
+  auto tmem = [&](int i, int e) -> R { return tr0[tstage(i) * 2 * NC * HB + e * HB]; };
   auto tissue = [&](int i) {   // thread 0: pair i's compact entries of both blocks
     if (threadIdx.x != 0 || i < 0) return;
     const uint32_t bytes = NC * HB * sizeof(R);
-    uint64_t* bar = &tbar[i & 1];
+    const int sg = tstage(i);
+    uint64_t* bar = &tbar[sg];
     mbar_expect_tx(bar, 2 * bytes);
     const int64_t b0 = (int64_t)blockIdx.x * 2;
     for (int j = 0; j < 2; ++j)
-      bulk_g2s(tring + ((i & 1) * 2 + j) * NC * HB, scratch + (int64_t)i * LN::pair_stride(M) + (b0 + j) * LN::SE * HB,
+      bulk_g2s(tring + (sg * 2 + j) * NC * HB, scratch + (int64_t)i * LN::pair_stride(M) + (b0 + j) * LN::SE * HB,
                bytes, bar);
   };
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
-      mbar_init(&tbar[0], 1);
-      mbar_init(&tbar[1], 1);
+      for (int k = 0; k < NS; ++k) mbar_init(&tbar[k], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    tissue(N - 1);
+    for (int k = 0; k < NS - 1; ++k) tissue(N - 1 - k);
   }
   const LineCell<DIM, PER, R> lc(ix, cx.h, m, o0, o1, o2, mod, m1, m2);
   const auto& cg = lc.cg;
@@ -1293,7 +1307,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
         for (int q = 0; q < B; ++q) in.yu[q] = tmem(i + 1, LN::Y0C + q);
       }
       __syncthreads();
-      tissue(i - 1);
+      tissue(i - (NS - 1));   // into pair i+1's stage, which every thread has left
       if (i + 1 < N) load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i + 1), in.VC);
       if (i + 1 < N) {
 #pragma unroll
@@ -1309,7 +1323,7 @@ __global__ void __launch_bounds__(128, CMP ? SMK_BACK_MINB : 1) k_scgs_back(KktC
       if (i >= 0) {
         in.fpb = so.PB + (int64_t)i * cx.nc;
         in.pbo = in.fpb[L.co];
-        mbar_wait(&tbar[i & 1], (uint32_t)(((N - 1 - i) >> 1) & 1));
+        mbar_wait(&tbar[tstage(i)], (uint32_t)(((N - 1 - i) / NS) & 1));
 #pragma unroll
         for (int e = 0; e < NTT; ++e) in.t[e] = tmem(i, LN::T0 + e);
 #pragma unroll
@@ -1770,13 +1784,18 @@ struct Nso : NsoBase {
     return (R*)p;
   }
 
-  // forward-kernel shape thresholds (colour cells): >= fwd_big -> TM 64 / P 1,
-  // >= fwd_mid -> TM 32 / P 2, else TM 32 / P 4.  SMK_FWD_THRESH="big,mid"
-  // overrides them (tuning runs only).  The 64^3 red-black colours (131,072
-  // cells: cfg5 level 1, cfg4 level 0) run TM 32 / P 2: 3.5 waves of TM 64
-  // CTAs left a half-empty last wave (level-1 forward 17.1 -> 12.6 ms per
-  // cfg5 V-cycle, backward 6.4 -> 5.3 ms with the factored hand-off).
-  int64_t fwd_big = 148 * 64 * 16, fwd_mid = 148 * 32 * 2;
+  // forward-kernel shape thresholds (colour cells): >= fwd_big -> TM 64 (fp32:
+  // P 2, 168 registers, 2 CTAs / SM; fp64: P 1), >= fwd_mid -> TM 32 / P 2,
+  // else TM 32 / P 4.  SMK_FWD_THRESH="big,mid" overrides them (tuning runs
+  // only).  The 64^3 red-black colours (131,072 cells: cfg5 level 1, cfg4
+  // level 0) take the TM 64 / P 2 shape with the factored hand-off (cfg5
+  // level-1 forward 11.2 -> 9.1 ms per V-cycle vs TM 32 / P 2; TM 64 / P 1
+  // there: 14.4 ms; the compact hand-off: forward 8.9 but backward 4.7 -> 5.3).
+  int64_t fwd_big = 148 * 64 * 10, fwd_mid = 148 * 32 * 2;
+  // shape-0 colours with >= cmp_min cells hand off the compact format
+  // (SMK_CMP_MIN overrides)
+  int64_t cmp_min = 148 * 64 * 16;
+  bool fwd_p1 = false;   // SMK_FWD_P1=1: fp32 TM 64 colours on one producer group
   // backward: colours with >= back_flat cells use the unpipelined variant
   // (occupancy), smaller ones the load-pipelined one.  SMK_BACK_FLAT overrides.
   int64_t back_flat = 148 * 128 * 4;
@@ -1784,7 +1803,9 @@ struct Nso : NsoBase {
   bool back_deep = getenv("SMK_BACK_DEEP") == nullptr || atoi(getenv("SMK_BACK_DEEP")) != 0;
 
   Nso(const Geo& g, const smk_nso_params& p) : prm(p) {
-    if (const char* e = getenv("SMK_BACK_FLAT")) back_flat = atoll(e);
+    if (const char* e = getenv("SMK_BACK_FLAT")) cmp_min = back_flat = atoll(e);   // tuning / tests: compact from back_flat up
+    if (const char* e = getenv("SMK_CMP_MIN")) cmp_min = atoll(e);
+    if (const char* e = getenv("SMK_FWD_P1")) fwd_p1 = atoi(e) != 0;
 
     if (const char* e = getenv("SMK_FWD_THRESH")) {
       long long a = 0, b = 0;
@@ -2089,7 +2110,7 @@ struct Nso : NsoBase {
     int shape = M >= fwd_big ? 0 : (M >= fwd_mid ? 1 : 2);
     // big colours (unpipelined backward) hand off the compact D~ / rhs
     // format, small latency-bound ones the factored format
-    const bool cmp = M >= back_flat && shape == 0;
+    const bool cmp = M >= back_flat && M >= cmp_min && shape == 0;
     if (shape == 2) {
       if (back_deep) launch_fwd<32, 4, 0, 2>(c, r, rhs != nullptr, o, mod, mm, M, st);
       else launch_fwd<32, 4, 0, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
@@ -2097,6 +2118,14 @@ struct Nso : NsoBase {
       with_nx(l, [&](auto nxc) {
         constexpr int NXv = decltype(nxc)::value;
         if (shape == 0) {
+          // fp32 compact colours: two producer groups, 2 CTAs / SM at 168
+          // registers (cfg5 level-0 forward 60.9 -> 58.2 ms per V-cycle;
+          // P = 3 and producer-side prep measured slower: 72.0 / 67.7 ms);
+          // SMK_FWD_P1=1 keeps the one-group shape
+          if constexpr (sizeof(R) == 4) {
+            if (cmp && !fwd_p1) return launch_fwd<64, 2, NXv, 1>(c, r, rhs != nullptr, o, mod, mm, M, st);
+            if (!cmp && !fwd_p1) return launch_fwd<64, 2, NXv, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
+          }
           if (cmp) launch_fwd<64, 1, NXv, 1>(c, r, rhs != nullptr, o, mod, mm, M, st);
           else launch_fwd<64, 1, NXv, 0>(c, r, rhs != nullptr, o, mod, mm, M, st);
         } else {

@@ -194,8 +194,13 @@ def test_scgs_sweep_every_kernel_shape(nso, shape_env, fwd, back, dim, bnd, rb):
     assert state_err(dev, want) < 1e-10
 
 
-@pytest.mark.parametrize("fwd", list(SHAPES))
-def test_fp32_sweep_every_kernel_shape(nso, shape_env, fwd):
+@pytest.mark.parametrize("fwd", list(SHAPES) + ["tm64p1-one-group"])
+def test_fp32_sweep_every_kernel_shape(nso, shape_env, monkeypatch, fwd):
+    # fp32 TM 64 colours run two producer groups by default; SMK_FWD_P1=1
+    # keeps the one-group shape (fp64's) reachable
+    if fwd == "tm64p1-one-group":
+        monkeypatch.setenv("SMK_FWD_P1", "1")
+        fwd = "tm64p1"
     shape_env(fwd, 0)
     pb = make_problem(3, n=8, N=4, seed=52)
     s, cfg = spec_cfg(nso, pb)

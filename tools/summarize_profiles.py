@@ -18,6 +18,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "l1tex__m_xbar2l1tex_read_bytes.sum", "l1tex__m_l1tex2xbar_write_bytes.sum",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
@@ -52,11 +55,23 @@ def main(tag, cfg, kernel="k_scgs_fwd"):
         f.write(f"# ncu launch list, one timed V-cycle of bench.py --config {cfg} (--profile-from-start off)\n")
         f.write("# kernel grid | launches | total | per launch | share | DRAM GB/s (bytes/duration)\n")
         f.write(summ)
-    rep = os.path.join(out, f"{tag}_c{cfg}_top.ncu-rep")
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    full_summary(tag, os.path.join(out, f"{tag}_c{cfg}_top"), os.path.join(prof, f"{tag}_c{cfg}_{kernel}_L0_ncu_full.csv"))
+    if os.path.exists(os.path.join(out, f"{tag}_back_raw.csv")):
+        full_summary(tag, os.path.join(out, f"{tag}_back"), os.path.join(prof, f"{tag}_c{cfg}_k_scgs_back_L0_ncu_full.csv"))
+    print(open(os.path.join(prof, f"{tag}_c{cfg}_launch_summary.txt")).read())
+
+
+def full_summary(tag, stem, dst):
+    """key metrics + stall reasons of one ncu --set full capture: <stem>.ncu-rep,
+    or its raw page already exported on the GPU box as <stem>_raw.csv"""
+    if os.path.exists(stem + "_raw.csv"):
+        raw = open(stem + "_raw.csv").read()
+    else:
+        raw = subprocess.run(["ncu", "-i", stem + ".ncu-rep", "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
     h, units, r = rr[0], rr[1], rr[2]
-    with open(os.path.join(prof, f"{tag}_c{cfg}_{kernel}_L0_ncu_full.csv"), "w", newline="") as f:
+    with open(dst, "w", newline="") as f:
         w = csv.writer(f)
         w.writerow(["metric", "unit", "value"])
         w.writerow(["Kernel Name", "", r[h.index("Kernel Name")]])
@@ -69,7 +84,6 @@ def main(tag, cfg, kernel="k_scgs_fwd"):
         for v, k in sorted(st, reverse=True)[:10]:
             w.writerow([k.replace("smsp__pcsamp_warps_issue_stalled_", "stall_"), "% of samples",
                         f"{100 * v / tot:.1f}"])
-    print(open(os.path.join(prof, f"{tag}_c{cfg}_launch_summary.txt")).read())
 
 
 if __name__ == "__main__":
