@@ -1225,8 +1225,8 @@ struct BackIn {
 // TMA (compact + fused, 128-thread CTAs = two 64-cell hand-off blocks, the
 // host launches it only when the colour is a multiple of 128 cells): the
 // compact entries of pair i for the CTA's two blocks (2 x 35 x 64 values,
-// contiguous per block) arrive by two 1D bulk async copies issued one step
-// ahead by thread 0 into a 2-stage shared-memory ring, completion on an
+// contiguous per block) arrive by two 1D bulk async copies issued NS - 1 steps
+// ahead by thread 0 into an NS-stage shared-memory ring (fp32: 3), completion on an
 // mbarrier per stage; the thread reads its t / b / yu from shared memory, so
 // the 42 hand-off loads per step and their address math leave the serial
 // chain.  One __syncthreads per step frees the stage the next copy targets.
