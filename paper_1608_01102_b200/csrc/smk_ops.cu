@@ -572,10 +572,15 @@ __global__ void __launch_bounds__(32 * kProlongWarps) k_prolong_face(Ix<DIM, PER
 // ===========================================================================
 
 // out = s * T(v) x  (T from advection.py:88-97); optional acc += out and
-// max |out| reduction.  v has `vframes` frames (1 = broadcast).
+// max |out| reduction.  v has `vframes` frames (1 = broadcast).  `gate`: the
+// previous Taylor term's norm -- a term launched speculatively past the
+// adaptive stop (*gate < gate_tol, advection.py:157-160) is a no-op and leaves
+// its own norm slot at 0, so every later term is skipped too.
 template <int DIM, bool PER, class R>
 __global__ void k_transport(Ix<DIM, PER> ix, R c0, Face3<R> v, int vframes, const R* __restrict__ x,
-                            R* __restrict__ out, R s, R* __restrict__ acc, R* norm, int N) {
+                            R* __restrict__ out, R s, R* __restrict__ acc, R* norm, int N,
+                            const R* gate = nullptr, R gate_tol = R(0)) {
+  if (gate && *gate < gate_tol) return;
   const int64_t nc = ix.cells();
   R m = R(0);
   SMK_GRID_STRIDE(t, (int64_t)N * nc) {
@@ -1345,13 +1350,17 @@ int project(const Geo& g, Face3<R> in, FaceW<R> out, double tol, int* cycles, do
   return rc2 ? rc2 : rc;
 }
 
-// Taylor exp(+-T dt) x (advection.py:144-174).  One launch per term; the
-// adaptive stop needs the term's inf-norm on the host (one sync per term).
+// Taylor exp(+-T dt) x (advection.py:144-174).  One launch per term.  The
+// adaptive stop (first term with |term|inf < tol) is decided on the device:
+// terms are launched in speculative batches, each gated on its predecessor's
+// norm, and the host reads the norms once per batch (normally once per call:
+// the first batch is as long as the previous call's order).
 template <int DIM, bool PER, class R>
 int advect(const Geo& g, Face3<R> v, const R* rho, R* out, double dt, double tol, int cap, int k_fixed,
            int transpose, int* k_used, double* last, cudaStream_t st) {
   Ix<DIM, PER> ix(g);
   int64_t n = ix.cells();
+  if (cap < 1) { set_error("advect: term cap must be >= 1"); return SMK_ERR_ARG; }
   Scratch sc(st);
   R* t0 = (R*)sc.get(n * sizeof(R));
   R* t1 = (R*)sc.get(n * sizeof(R));
@@ -1363,45 +1372,41 @@ int advect(const Geo& g, Face3<R> v, const R* rho, R* out, double dt, double tol
   R* bufs[2] = {t0, t1};
   R c0 = (R)(0.5 / g.h);
   int gb = grid_for(n, 256);
-  double nrm = 0.0;
-  for (int k = 1;; ++k) {
-    if (k > cap) {
-      R lastv = 0;
-      cudaMemcpyAsync(&lastv, norms + (k - 2), sizeof(R), cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      if (last) *last = (double)lastv;
-      if (k_used) *k_used = cap;
-      set_error("Taylor term cap %d exceeded (dt*|v|/h too large)", cap);
-      return SMK_TRUNCATION_OVERFLOW;
+  const bool adaptive = k_fixed <= 0;
+  const int kmax = adaptive ? cap : (k_fixed < cap ? k_fixed : cap);
+  static thread_local int hint = 6;
+  std::vector<R> hn((size_t)cap + 2, R(0));
+  int k = 0;  // terms launched so far
+  while (k < kmax) {
+    int upto = adaptive ? (k == 0 ? hint : k + 4) : kmax;
+    if (upto > kmax) upto = kmax;
+    for (++k; k <= upto; ++k) {
+      R s = (R)(dt / (double)k);
+      if (transpose) s = -s;
+      R* nxt = bufs[(k - 1) & 1];
+      // reference: term = (dt/k) * stencil(term) with stencil = +-T
+      const R* gate = adaptive && k >= 2 ? norms + (k - 2) : nullptr;
+      k_transport<DIM, PER, R><<<gb, 256, 0, st>>>(ix, c0, v, 1, cur, nxt, s, out, norms + (k - 1), 1, gate, (R)tol);
+      count_launch();
+      cur = nxt;
     }
-    R s = (R)(dt / (double)k);
-    if (transpose) s = -s;
-    R* nxt = bufs[(k - 1) & 1];
-    // reference: term = (dt/k) * stencil(term) with stencil = +-T
-    k_transport<DIM, PER, R><<<gb, 256, 0, st>>>(ix, c0, v, 1, cur, nxt, s, out, norms + (k - 1), 1); count_launch();
-    cur = nxt;
-    if (k_fixed > 0) {
-      if (k == k_fixed) {
-        R lastv = 0;
-        cudaMemcpyAsync(&lastv, norms + (k - 1), sizeof(R), cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
-        nrm = (double)lastv;
-        if (k_used) *k_used = k;
-        if (last) *last = nrm;
+    k = upto;
+    cudaMemcpyAsync(hn.data(), norms, sizeof(R) * (size_t)k, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (!adaptive) break;
+    for (int j = 1; j <= k; ++j)
+      if (hn[j - 1] < (R)tol) {  // the device gate's comparison, same rounding
+        hint = j;
+        if (k_used) *k_used = j;
+        if (last) *last = (double)hn[j - 1];
         return cuda_check("advect");
       }
-      continue;
-    }
-    R lastv = 0;
-    cudaMemcpyAsync(&lastv, norms + (k - 1), sizeof(R), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    nrm = (double)lastv;
-    if (nrm < tol) {
-      if (k_used) *k_used = k;
-      if (last) *last = nrm;
-      return cuda_check("advect");
-    }
   }
+  if (last) *last = (double)hn[kmax - 1];
+  if (k_used) *k_used = kmax;
+  if (!adaptive && k_fixed <= cap) return cuda_check("advect");
+  set_error("Taylor term cap %d exceeded (dt*|v|/h too large)", cap);
+  return SMK_TRUNCATION_OVERFLOW;
 }
 
 template <int DIM, bool PER, class R>

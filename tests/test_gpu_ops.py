@@ -132,6 +132,35 @@ def test_taylor_overflow_maps_to_exception(smk):
         A.advect_scalar(s, v, rng.standard_normal(s.res), 10.0, cap=16)
 
 
+def test_taylor_speculative_batches_keep_the_adaptive_stop(smk):
+    """The adaptive Taylor stop (``advection.py:144-163``) is decided on the
+    device: terms are launched in speculative batches gated on the previous
+    term's norm.  A short line after a long one (over-launched, gated terms)
+    and a long one after a short one (several batches) must give the oracle's
+    order and the same bits as the fixed-order evaluation."""
+    from oracle import ops
+    from oracle.grid import Grid
+    _, F, A, _ = smk
+    s = F.GridSpec(2, (16, 16), 1 / 16, "neumann")
+    g = Grid(2, (16, 16), 1 / 16, "neumann")
+    rng = np.random.default_rng(10)
+    v = F.zero_boundary_faces(s, tuple(rng.standard_normal(s.face_shape(k)) for k in range(2)))
+    rho = rng.standard_normal(s.res)
+    orders = []
+    for dt in (0.002, 0.2, 0.0005, 0.1, 0.3, 0.001):
+        out, rep = A.advect_scalar(s, v, rho, dt)
+        want, k_ref, _ = ops.taylor(g, v, rho, dt, tol=A.DEFAULT_TRUNCATION_TOL, cap=A.DEFAULT_TERM_CAP)
+        assert rep.k_used == k_ref
+        assert rel_err(out, want) < 1e-13
+        fixed, _ = A.advect_scalar(s, v, rho, dt, k_fixed=rep.k_used)
+        assert np.array_equal(out, fixed)
+        back, repT = A.advect_scalar_rho_T(s, v, rho, dt)
+        backf, _ = A.advect_scalar_rho_T(s, v, rho, dt, k_fixed=repT.k_used)
+        assert np.array_equal(back, backf)
+        orders.append(rep.k_used)
+    assert max(orders) >= min(orders) + 8   # the sequence really alternates short and long lines
+
+
 def test_determinism(smk):
     _, F, A, _ = smk
     s = F.GridSpec(2, (16, 16), 1 / 16, "neumann")
