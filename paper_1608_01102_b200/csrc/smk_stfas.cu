@@ -2557,6 +2557,7 @@ struct Slabs : SlabsBase {
   Scratch mem;
   int64_t nbytes = 0;
   ncclComm_t comm = nullptr;
+  bool nccl_local = false;   // SMK_SLABS_NCCL_LOCAL=1: local-neighbour halos by NCCL self send / recv
   // per level: pinned v0 (slab 0), per local slab: halo frames and guide
   struct H {
     R* vprev[3] = {nullptr, nullptr, nullptr};
@@ -2615,7 +2616,10 @@ struct Slabs : SlabsBase {
     }
     dnorm = (double*)mem.get(sizeof(double) * 2 * (nloc + 1));
     if (!dnorm) ok = false;
-    if (world > 1) {
+    // a communicator whenever a unique id is given: world > 1 needs one; a
+    // one-rank world takes it too (norm allreduce over NCCL -- the path a
+    // single-GPU box can exercise, tests/test_gpu_slabs.py)
+    if (world > 1 || nccl_id) {
       if (!nccl_id || !g_nccl.load()) {
         set_error("slabs: world > 1 needs NCCL (libnccl.so.2) and a unique id");
         ok = false;
@@ -2628,6 +2632,8 @@ struct Slabs : SlabsBase {
         comm = nullptr;
         ok = false;
       }
+      const char* e = getenv("SMK_SLABS_NCCL_LOCAL");   // tests: local halos over NCCL too
+      nccl_local = e && atoi(e) != 0;
     }
   }
   ~Slabs() override {
@@ -2683,6 +2689,25 @@ struct Slabs : SlabsBase {
   // U from su[k]); remote neighbours over NCCL
   void exchange(int l, const std::vector<StP<R>>& sv, cudaStream_t st) {
     const auto& Lv = E[0]->lv[l];
+    if (comm && nccl_local) {
+      // local neighbours through NCCL self send / recv (matched in issue
+      // order inside one group): the halo path of a remote neighbour --
+      // ncclSend / ncclRecv captured into the V-cycle graph -- on one GPU
+      const ncclDataType_t ty = sizeof(R) == 8 ? ncclFloat64 : ncclFloat32;
+      g_nccl.GroupStart();
+      for (int k = 0; k < nloc; ++k)
+        for (int c = 0; c < DIM; ++c) {
+          if (k > 0) {
+            g_nccl.Send(sv[k - 1].V[c] + (int64_t)(ns[k - 1] - 1) * Lv.nf[c], (size_t)Lv.nf[c], ty, rank, comm, st);
+            g_nccl.Recv(hl[l][k].vprev[c], (size_t)Lv.nf[c], ty, rank, comm, st);
+          }
+          if (k < nloc - 1) {
+            g_nccl.Send(sv[k + 1].U[c], (size_t)Lv.nf[c], ty, rank, comm, st);
+            g_nccl.Recv(hl[l][k].unext[c], (size_t)Lv.nf[c], ty, rank, comm, st);
+          }
+        }
+      g_nccl.GroupEnd();
+    } else
     for (int k = 0; k < nloc; ++k) {
       if (k > 0)
         for (int c = 0; c < DIM; ++c)
@@ -2910,7 +2935,7 @@ struct Slabs : SlabsBase {
       mx = std::isnan(h[2 * k + 1]) ? h[2 * k + 1] : std::max(mx, h[2 * k]);
       sq += h[2 * k + 1];
     }
-    if (world > 1 && comm) {
+    if (comm) {
       double both[2] = {mx, sq};
       double* d = dnorm + 2 * nloc;
       cudaMemcpyAsync(d, both, sizeof(both), cudaMemcpyHostToDevice, st);

@@ -168,3 +168,47 @@ def test_c_four_slabs_converge_to_single_slab_solution():
     assert err <= 1e-8 * scale
     one.close()
     four.close()
+
+
+def test_c_slabs_over_a_one_rank_nccl_world(monkeypatch):
+    """The NCCL branch of the C++ slab set on the one GPU a test box has: a
+    one-rank world (unique id from libsmk's dlopen'ed NCCL, broadcast by
+    NcclSlabComm over a world_size-1 process group) creates a communicator
+    with ncclCommInitRank on the device and reduces the stop-test norms
+    through ncclAllReduce on the compute stream.  With SMK_SLABS_NCCL_LOCAL=1
+    the halos between the local slabs travel by ncclSend / ncclRecv (to the
+    rank itself) inside the captured V-cycle graph -- the remote-neighbour
+    path, first V-cycle captured, the others replayed.  Both must equal the
+    same slabs without NCCL bit for bit.  (A neighbour on another GPU needs a
+    second GPU: the driver's scaling run.)"""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1608_01102_b200.slabs import NcclSlabComm, build_c_solver
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = NcclSlabComm()
+        assert (comm.rank, comm.world) == (0, 1) and len(comm.uid) == 128 and any(comm.uid)
+        pb = make_problem(3, n=8, N=7, seed=213)
+        spec, cfg, (plain, pst) = c_setup(pb, [0, 1, 2], 3, 2)
+        nc, nst = build_c_solver(spec, cfg, pb.v0, pb.vstar, [0, 1, 2], 3, pb.N, torch.float64, comm=comm)
+        monkeypatch.setenv("SMK_SLABS_NCCL_LOCAL", "1")
+        lb, lst = build_c_solver(spec, cfg, pb.v0, pb.vstar, [0, 1, 2], 3, pb.N, torch.float64, comm=NcclSlabComm())
+        monkeypatch.delenv("SMK_SLABS_NCCL_LOCAL")
+        for _ in range(3):
+            for sv, st in ((plain, pst), (nc, nst), (lb, lst)):
+                sv.vcycle(st)
+                sv.gauge(st)
+        for a, b, c in zip(nst, pst, lst):
+            assert np.array_equal(flat_dev(a), flat_dev(b))
+            assert np.array_equal(flat_dev(c), flat_dev(b))
+        assert nc.norms(nst) == plain.norms(pst) == lb.norms(lst)
+        for sv in (lb, nc, plain):
+            sv.close()
+    finally:
+        dist.destroy_process_group()

@@ -96,3 +96,42 @@ def test_gloo_two_ranks_equal_in_process_slabs(tmp_path):
         got = np.load(os.path.join(tmp_path, f"rank{r}.npy"))
         assert np.array_equal(got, flat(states[r]))
         assert np.allclose(np.load(os.path.join(tmp_path, f"hist{r}.npy")), hist, rtol=1e-14, atol=0)
+
+
+def test_nccl_loader_and_unique_id():
+    """libsmk loads NCCL with dlopen and resolves every entry point the C++
+    slab set calls (smk_stfas.cu NcclApi); rank 0's unique id is 128 bytes,
+    not all zero, and differs between calls."""
+    import ctypes
+    from paper_1608_01102_b200 import _lib
+    L = _lib.load()
+    ids = []
+    for _ in range(2):
+        raw = (ctypes.c_ubyte * 128)()
+        _lib.check(L.smk_nccl_unique_id(ctypes.cast(raw, ctypes.c_void_p), 128), "nccl_unique_id")
+        ids.append(bytes(raw))
+    assert any(ids[0]) and ids[0] != ids[1]
+    small = (ctypes.c_ubyte * 16)()
+    assert L.smk_nccl_unique_id(ctypes.cast(small, ctypes.c_void_p), 16) == _lib.SMK_ERR_ARG
+
+
+def _uid_main(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1608_01102_b200.slabs import NcclSlabComm
+    comm = NcclSlabComm()
+    assert (comm.rank, comm.world) == (rank, world)
+    with open(os.path.join(out_dir, f"uid{rank}.bin"), "wb") as f:
+        f.write(comm.uid)
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_reaches_every_rank(tmp_path):
+    """NcclSlabComm: rank 0's id broadcast over torch.distributed (gloo here,
+    world_size 2) -- both ranks hand the same 128 bytes to smk_slabs_create."""
+    port = _free_port()
+    mp.spawn(_uid_main, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    a = open(os.path.join(tmp_path, "uid0.bin"), "rb").read()
+    b = open(os.path.join(tmp_path, "uid1.bin"), "rb").read()
+    assert len(a) == 128 and any(a) and a == b
