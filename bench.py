@@ -331,6 +331,8 @@ def main():
     ap.add_argument("--levels", type=int, default=0, help="hierarchy depth (0 = the config's)")
     ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution solves")
     ap.add_argument("--tts-budget", type=int, default=80)
+    ap.add_argument("--slabs", type=int, default=0,
+                    help="single process: S in-process time slabs on the C++ slab set (the N > 1 code path on one GPU)")
     args = ap.parse_args()
 
     import torch
@@ -358,29 +360,34 @@ def main():
     cfg = nso.StfasConfig(dt=w.dt, K=w.K, r=w.r, n_levels=args.levels or w.levels)
     stream = torch.cuda.current_stream()
     slab = None
-    if world > 1:
+    n_slabs = world if world > 1 else max(1, args.slabs)
+    if n_slabs > 1:
+        # one slab per rank (NCCL halos), or --slabs S in-process slabs on one GPU
         from paper_1608_01102_b200 import slabs
-        slab, slab_states = slabs.build_c_solver(spec, cfg, v0, vstar, [rank], world, w.N, w.dtype,
-                                                 comm=slabs.NcclSlabComm())
-        state = slab_states[0]
+        ids = [rank] if world > 1 else list(range(n_slabs))
+        slab, states = slabs.build_c_solver(spec, cfg, v0, vstar, ids, n_slabs, w.N, w.dtype,
+                                            comm=slabs.NcclSlabComm() if world > 1 else None)
         hier = slab                      # same profiling interface, summed over the local slabs
-        slab_t0, n_local = slab.frames[0]
+        slab_t0 = slab.frames[0][0]
+        n_local = sum(n for _, n in slab.frames)
     else:
         state = nso.SpacetimeState.zeros(spec, w.N, w.dtype)
         hier = nso.StfasHierarchy(spec, cfg, w.N, w.dtype)
         hier.set_guide(v0, vstar)
         n_local = w.N
+        states = [state]
 
     def step():
         if slab is not None:
-            slab.vcycle([state])
-            slab.gauge([state])
+            slab.vcycle(states)
+            slab.gauge(states)
         else:
             hier.vcycle(state)
             hier.gauge_fix(state)
 
     # inputs larger than L2 (126 MB) for configs >= 3; otherwise flush L2
-    state_bytes = sum(t.numel() * t.element_size() for t in (*state.V, state.PB, *state.U, state.P))
+    state_tensors = [t for st in states for t in (*st.V, st.PB, *st.U, st.P)]
+    state_bytes = sum(t.numel() * t.element_size() for t in state_tensors)
     guide_bytes = sum(t.numel() * t.element_size() for t in vstar) * n_local // w.N
     flush = None
     if state_bytes + guide_bytes < 4 * 126e6:
@@ -433,7 +440,7 @@ def main():
         ms = float(t.item())
 
     if slab is not None:
-        ri, r2 = slab.norms([state])
+        ri, r2 = slab.norms(states)
     else:
         ri, r2 = hier.residual_norms(state)
     value = w.cell_timesteps / (ms / 1000.0)   # strong scaling: the whole volume per V-cycle
@@ -450,7 +457,7 @@ def main():
     k_avg_ms = k_ms / max(k_n, 1)
     k_bytes_launch = (k_cells / max(k_n, 1)) * sweep_values(w.dim) * esz
     k_achieved = k_bytes_launch / (k_avg_ms / 1000.0) / 1e9 if k_n else 0.0
-    traffic = traffic_ref(w.name, kname)
+    traffic = traffic_ref(w.name, kname) if slab is None else None   # the capture is of the whole time line
     kernels = {}
     for k, v in kprof.items():
         kernels[k] = {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[1] / prof_steps,
@@ -467,13 +474,13 @@ def main():
         # device-timed, max over ranks
         pin = lambda t: t.detach().cpu().pin_memory()
         if slab is None:
-            d_in = list(vstar) + [t for t in (*state.V, state.PB, *state.U, state.P)]
+            d_in = list(vstar) + state_tensors
         else:
             # this rank's guide frames v*_{t0} .. v*_{t0+n} (uploaded into the
             # full guide tensor, re-bound by set_guide inside the timed region)
             t1 = min(slab_t0 + n_local + 1, w.N)
-            d_in = [c[slab_t0:t1] for c in vstar] + [t for t in (*state.V, state.PB, *state.U, state.P)]
-        d_st = [t for t in (*state.V, state.PB, *state.U, state.P)]
+            d_in = [c[slab_t0:t1] for c in vstar] + state_tensors
+        d_st = state_tensors
         h_in = [pin(t) for t in d_in]
         out_h = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in d_st]
         h2d = sum(t.numel() * t.element_size() for t in h_in)
@@ -522,12 +529,12 @@ def main():
     # (coarsest 4^d: the coarsest-level 10-sweep solve is what limits the
     # config's convergence factor)
     tts = None
-    if world == 1 and not args.no_tts:
+    if slab is None and not args.no_tts:
         tts = {"config_levels": time_to_solution(nso, spec, w, v0, vstar, w.levels, args.tts_budget),
                "full_depth": time_to_solution(nso, spec, w, v0, vstar, 99, args.tts_budget)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and slab is None and not args.no_cpu:
         try:
             rate, sec, sh, nt = cpu_vcycle_rate(w, 1)
             cpu = {"value": rate, "unit": "cell-updates/s", "cores": nt, "kind": "port",
@@ -544,7 +551,8 @@ def main():
             "dtype": "f32" if w.dtype == torch.float32 else "f64", "data": "synthetic",
             "config": {"workload": w.name, "config_index": w.index, "grid": f"{w.n}^{w.dim}", "frames": w.N,
                        "levels": hier.levels, "cell_timesteps": w.cell_timesteps,
-                       "parallelism": f"time-slabs x{world}" if world > 1 else "single",
+                       "parallelism": (f"time-slabs x{world}" if world > 1 else
+                                       f"time-slabs x{n_slabs} in-process" if slab is not None else "single"),
                        "l2": "flushed" if flush is not None else "inputs larger than L2",
                        "residual_inf_after": ri},
             "roofline": {"bound": "hbm", "kernel": f"{kname} (level 0)", "achieved": k_achieved, "peak": hbm,
