@@ -300,7 +300,7 @@ def e2e_pipelined(args, spec, cfg, w, v0, vstar, state, hier, h_in, out_h):
     for k in range(nl):
         call(k, done)
     torch.cuda.synchronize()
-    reps = max(4 * nl, args.steps)   # a stream of calls: fill + drain amortised over 12
+    reps = max(8 * nl, args.steps)   # a stream of calls: fill (one upload) + drain (one download) amortised over 24
     done = [None] * nl
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
