@@ -214,13 +214,38 @@ __device__ __forceinline__ void pair_rows(const KktCtx<DIM, PER, R>& cx, const L
 // reduced in a fixed order by k_norm_final -- every residual entry is
 // produced by exactly one thread, so this is ||f||_inf / ||f||_2 of the full
 // residual without writing it (5.4 GB at cfg5) and reading it back.
+// Each thread walks its cell through `fpt` consecutive frames (blockIdx.z =
+// frame group): the cell's index math, wall flags and offsets are formed
+// once, and V_{i-1} at the own faces is carried from the previous frame's
+// register cache instead of being loaded again (the same values: results are
+// bitwise those of one thread per cell-frame).  cfg5 level 0: 6.0 -> 5.4 ms,
+// the stop test 6.7 -> 4.8 ms (fpt 8; 4: 5.7 / 5.3; 2: 6.4 / 6.0).
+#ifndef SMK_KKT_FPT
+#define SMK_KKT_FPT 8
+#endif
+// frames per thread: SMK_KKT_FPT on levels of >= 64^3 cells while the launch
+// still has >= 8 blocks per SM, else 1 (smaller levels and the 2D configs are
+// latency-bound and measured slower with a frame loop: 32^3 0.24 -> 0.33 ms,
+// 256^2 0.13 -> 0.17 ms)
+inline int kkt_fpt(int64_t nc, int nframes) {
+  if (nc < 262144) return 1;
+  int fpt = SMK_KKT_FPT;
+  const int64_t bpf = (nc + 255) / 256;
+  while (fpt > 1 && bpf * ((nframes + fpt - 1) / fpt) < 148 * 8) fpt >>= 1;
+  return fpt;
+}
+inline dim3 kkt_grid(int64_t nc, int nframes) {
+  const int fpt = kkt_fpt(nc, nframes);
+  return frame_grid(nc, (nframes + fpt - 1) / fpt, 256);
+}
 template <int DIM, bool PER, class R, bool HR, int NX, bool NORM = false>
-__global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out,
-                                             double* __restrict__ part = nullptr) {
+__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out,
+                                             double* __restrict__ part = nullptr, int fpt = 1) {
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
-  const int i = blockIdx.z;
+  const int i0 = blockIdx.z * fpt;
+  const int i1 = i0 + fpt < cx.N ? i0 + fpt : cx.N;
   R mx = R(0);
   double sq = 0.0;
   auto put = [&](R* dst, int64_t o, R v) {
@@ -241,29 +266,36 @@ __global__ void __launch_bounds__(256) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs
       wall[2 * k] = !PER && c[k] == 0;
       wall[2 * k + 1] = !PER && c[k] == ix.n(k) - 1;
     }
-    R VC[DIM][NB], UC[DIM][NB];
-    load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i), VC);
-    load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.U, i), UC);
-    const Face3<R> Vp = i == 0 ? cx.v0 : cx.frame(cx.V, i - 1);
     R vp[NF];
+    {
+      const Face3<R> Vp = i0 == 0 ? cx.v0 : cx.frame(cx.V, i0 - 1);
 #pragma unroll
-    for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
-    R yu[B], yv[B];
-    pair_rows<DIM, PER, R, false, true, HR>(cx, L, wall, i, VC, UC, vp, rhs, yu, yv);
-#pragma unroll
-    for (int k = 0; k < DIM; ++k) {
-      const int64_t o = (int64_t)i * cx.nf[k] + L.of[2 * k];
-      put(out.R3[k], o, yu[2 * k]);
-      put(out.R1[k], o, yv[2 * k]);
-      if (!PER && wall[2 * k + 1]) {
-        const int64_t ou = (int64_t)i * cx.nf[k] + L.of[2 * k + 1];
-        put(out.R3[k], ou, HR ? R(0) - rhs.R3[k][ou] : R(0));
-        put(out.R1[k], ou, HR ? R(0) - rhs.R1[k][ou] : R(0));
-      }
+      for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
     }
-    const int64_t oc = (int64_t)i * nc + L.co;
-    put(out.R4, oc, yu[NF]);
-    put(out.R2, oc, yv[NF]);
+    for (int i = i0; i < i1; ++i) {
+      R VC[DIM][NB], UC[DIM][NB];
+      load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i), VC);
+      load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.U, i), UC);
+      R yu[B], yv[B];
+      pair_rows<DIM, PER, R, false, true, HR>(cx, L, wall, i, VC, UC, vp, rhs, yu, yv);
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        const int64_t o = (int64_t)i * cx.nf[k] + L.of[2 * k];
+        put(out.R3[k], o, yu[2 * k]);
+        put(out.R1[k], o, yv[2 * k]);
+        if (!PER && wall[2 * k + 1]) {
+          const int64_t ou = (int64_t)i * cx.nf[k] + L.of[2 * k + 1];
+          put(out.R3[k], ou, HR ? R(0) - rhs.R3[k][ou] : R(0));
+          put(out.R1[k], ou, HR ? R(0) - rhs.R1[k][ou] : R(0));
+        }
+      }
+      const int64_t oc = (int64_t)i * nc + L.co;
+      put(out.R4, oc, yu[NF]);
+      put(out.R2, oc, yv[NF]);
+      // V_i at the own lower faces is the next frame's V_{i-1} (slot 1 of the cache)
+#pragma unroll
+      for (int q = 0; q < NF; q += 2) vp[q] = VC[q >> 1][1];
+    }
   }
   if constexpr (NORM) {
     __shared__ double shm[8], shs[8];
@@ -1972,11 +2004,12 @@ struct Nso : NsoBase {
     auto c = ctx(l, s);
     ResP<R> r = rhs ? *rhs : ResP<R>{};
     prof_begin(2, l, lv[l].nc, st);
-    const dim3 grid = frame_grid(lv[l].nc, prm.n_frames, 256);
+    const dim3 grid = kkt_grid(lv[l].nc, prm.n_frames);
     with_nx(l, [&](auto nxc) {
       constexpr int NXv = decltype(nxc)::value;
-      if (rhs) k_kkt<DIM, PER, R, true, NXv><<<grid, 256, 0, st>>>(c, r, out);
-      else k_kkt<DIM, PER, R, false, NXv><<<grid, 256, 0, st>>>(c, r, out);
+      const int fpt = kkt_fpt(lv[l].nc, prm.n_frames);
+      if (rhs) k_kkt<DIM, PER, R, true, NXv><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
+      else k_kkt<DIM, PER, R, false, NXv><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
     });
     count_launch();
     prof_end(2, st);
@@ -2383,7 +2416,7 @@ struct Nso : NsoBase {
   // fixed-order reduction into dev_out[0..1] = {max |f|, sum f^2}
   int norm_launch(const StP<R>& top, double* dev_out, cudaStream_t st) {
     auto c = ctx(0, top);
-    const dim3 grid = frame_grid(lv[0].nc, prm.n_frames, 256);
+    const dim3 grid = kkt_grid(lv[0].nc, prm.n_frames);
     const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
     if (nparts_n < nblk + 1) {
       nparts = (double*)mem.get(sizeof(double) * 2 * (nblk + 1));
@@ -2393,7 +2426,8 @@ struct Nso : NsoBase {
     prof_begin(2, 0, lv[0].nc, st);
     with_nx(0, [&](auto nxc) {
       constexpr int NXv = decltype(nxc)::value;
-      k_kkt<DIM, PER, R, false, NXv, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts);
+      k_kkt<DIM, PER, R, false, NXv, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts,
+                                                                 kkt_fpt(lv[0].nc, prm.n_frames));
     });
     count_launch();
     prof_end(2, st);
@@ -2414,7 +2448,7 @@ struct Nso : NsoBase {
     if (!guide_set) { set_error("nso: set_guide not called"); return SMK_ERR_ARG; }
     int rc = norm_launch(from_api(s), nullptr, st);
     if (rc) return rc;
-    const dim3 grid = frame_grid(lv[0].nc, prm.n_frames, 256);
+    const dim3 grid = kkt_grid(lv[0].nc, prm.n_frames);
     const int64_t nblk = (int64_t)grid.x * grid.y * grid.z;
     double h[2] = {0.0, 0.0};
     int fl = 0;
