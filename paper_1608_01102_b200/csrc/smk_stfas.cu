@@ -238,14 +238,16 @@ inline dim3 kkt_grid(int64_t nc, int nframes) {
   const int fpt = kkt_fpt(nc, nframes);
   return frame_grid(nc, (nframes + fpt - 1) / fpt, 256);
 }
-template <int DIM, bool PER, class R, bool HR, int NX, bool NORM = false>
-__global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out,
+// FL: the frame-loop shape (fpt > 1); !FL is the one-thread-per-cell-frame
+// shape of the small levels, unchanged.
+template <int DIM, bool PER, class R, bool HR, int NX, bool NORM = false, bool FL = false>
+__global__ void __launch_bounds__(256, FL && sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM, PER, R> cx, ResP<R> rhs, ResP<R> out,
                                              double* __restrict__ part = nullptr, int fpt = 1) {
   constexpr int NF = 2 * DIM, B = NF + 1, NB = NbrSlots<DIM>::NB;
   const auto& ix = cx.ix;
   const int64_t nc = cx.nc;
-  const int i0 = blockIdx.z * fpt;
-  const int i1 = i0 + fpt < cx.N ? i0 + fpt : cx.N;
+  const int i0 = FL ? blockIdx.z * fpt : blockIdx.z;
+  const int i1 = FL ? (i0 + fpt < cx.N ? i0 + fpt : cx.N) : i0 + 1;
   R mx = R(0);
   double sq = 0.0;
   auto put = [&](R* dst, int64_t o, R v) {
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM,
       wall[2 * k + 1] = !PER && c[k] == ix.n(k) - 1;
     }
     R vp[NF];
-    {
+    if constexpr (FL) {
       const Face3<R> Vp = i0 == 0 ? cx.v0 : cx.frame(cx.V, i0 - 1);
 #pragma unroll
       for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
@@ -276,6 +278,11 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM,
       R VC[DIM][NB], UC[DIM][NB];
       load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.V, i), VC);
       load_nbr<DIM, PER, R>(ix, L, cx.frame(cx.U, i), UC);
+      if constexpr (!FL) {
+        const Face3<R> Vp = i == 0 ? cx.v0 : cx.frame(cx.V, i - 1);
+#pragma unroll
+        for (int q = 0; q < NF; ++q) vp[q] = (q & 1) ? R(0) : Vp.c[q >> 1][L.of[q]];
+      }
       R yu[B], yv[B];
       pair_rows<DIM, PER, R, false, true, HR>(cx, L, wall, i, VC, UC, vp, rhs, yu, yv);
 #pragma unroll
@@ -293,8 +300,10 @@ __global__ void __launch_bounds__(256, sizeof(R) == 4 ? 2 : 1) k_kkt(KktCtx<DIM,
       put(out.R4, oc, yu[NF]);
       put(out.R2, oc, yv[NF]);
       // V_i at the own lower faces is the next frame's V_{i-1} (slot 1 of the cache)
+      if constexpr (FL) {
 #pragma unroll
-      for (int q = 0; q < NF; q += 2) vp[q] = VC[q >> 1][1];
+        for (int q = 0; q < NF; q += 2) vp[q] = VC[q >> 1][1];
+      }
     }
   }
   if constexpr (NORM) {
@@ -2008,8 +2017,13 @@ struct Nso : NsoBase {
     with_nx(l, [&](auto nxc) {
       constexpr int NXv = decltype(nxc)::value;
       const int fpt = kkt_fpt(lv[l].nc, prm.n_frames);
-      if (rhs) k_kkt<DIM, PER, R, true, NXv><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
-      else k_kkt<DIM, PER, R, false, NXv><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
+      if (fpt > 1) {
+        if (rhs) k_kkt<DIM, PER, R, true, NXv, false, true><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
+        else k_kkt<DIM, PER, R, false, NXv, false, true><<<grid, 256, 0, st>>>(c, r, out, nullptr, fpt);
+      } else {
+        if (rhs) k_kkt<DIM, PER, R, true, NXv><<<grid, 256, 0, st>>>(c, r, out);
+        else k_kkt<DIM, PER, R, false, NXv><<<grid, 256, 0, st>>>(c, r, out);
+      }
     });
     count_launch();
     prof_end(2, st);
@@ -2426,8 +2440,9 @@ struct Nso : NsoBase {
     prof_begin(2, 0, lv[0].nc, st);
     with_nx(0, [&](auto nxc) {
       constexpr int NXv = decltype(nxc)::value;
-      k_kkt<DIM, PER, R, false, NXv, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts,
-                                                                 kkt_fpt(lv[0].nc, prm.n_frames));
+      const int fpt = kkt_fpt(lv[0].nc, prm.n_frames);
+      if (fpt > 1) k_kkt<DIM, PER, R, false, NXv, true, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts, fpt);
+      else k_kkt<DIM, PER, R, false, NXv, true><<<grid, 256, 0, st>>>(c, ResP<R>{}, ResP<R>{}, nparts);
     });
     count_launch();
     prof_end(2, st);

@@ -1,5 +1,5 @@
 #!/bin/bash
-# final-tree pass: smoke, per-config k_kkt / stop-test times, every GPU test, the default bench line
+# final-tree pass: smoke, the default bench line, cfg3 / cfg4 lines, every GPU test
 TAG=${1:-r02z}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke=$? | tee -a gpurun_out/${TAG}_smoke.log
@@ -8,5 +8,4 @@ timeout 700 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench.json 
 for C in 4 3 2 1; do
   timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-e2e > gpurun_out/${TAG}_c$C.json 2> gpurun_out/${TAG}_c$C.err; summ gpurun_out/${TAG}_c$C.json "cfg$C"
 done
-timeout 300 python bench.py --config 4 --dtype fp64 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/${TAG}_c4f64.json 2>/dev/null; summ gpurun_out/${TAG}_c4f64.json c4f64
 timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo pytest=$? >> gpurun_out/${TAG}_pytest_gpu.log; tail -3 gpurun_out/${TAG}_pytest_gpu.log
